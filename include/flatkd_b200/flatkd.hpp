@@ -1,0 +1,282 @@
+// flatkd_b200/flatkd.hpp — the reference's C++ query API over the B200 C ABI.
+//
+// Header-only shim mirroring flatkd (proj/include/flatkd/{point,tree,
+// traverse,batch}.hpp): same names, argument meanings, result layout and
+// exception types, in namespace flatkd::b200.  A caller switches by changing
+// the include and the namespace:
+//
+//   flatkd::BatchResult r = flatkd::run_batch(tree, queries, opts);          // CPU
+//   flatkd::b200::BatchResult r = flatkd::b200::run_batch(tree, queries, opts);  // B200
+//
+// Every query runs in the sm_100a kernels behind include/fkd_b200.h; there
+// is no host fallback.  When the reference headers are also included,
+// flatkd_b200/reference_adapter.hpp accepts the reference's own KdTree /
+// PointSet / BatchOptions and fills a flatkd::BatchResult directly.
+#pragma once
+
+#include <array>
+#include <cmath>
+#include <cstdint>
+#include <limits>
+#include <memory>
+#include <optional>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "fkd_b200.h"
+
+namespace flatkd::b200 {
+
+// error.hpp:9-18
+class DataError : public std::runtime_error {
+public:
+    explicit DataError(const std::string& what) : std::runtime_error(what) {}
+};
+
+class InvariantError : public std::runtime_error {
+public:
+    explicit InvariantError(const std::string& what) : std::runtime_error(what) {}
+};
+
+class DeviceError : public std::runtime_error {
+public:
+    explicit DeviceError(const std::string& what) : std::runtime_error(what) {}
+};
+
+inline void check(fkd_status s) {
+    if (s == FKD_OK) return;
+    const std::string msg = fkd_last_error();
+    switch (s) {
+        case FKD_INVALID_ARGUMENT: throw std::invalid_argument(msg);
+        case FKD_DATA_ERROR: throw DataError(msg);
+        case FKD_INVARIANT_ERROR: throw InvariantError(msg);
+        default: throw DeviceError(msg);
+    }
+}
+
+inline constexpr float kInfRadius = std::numeric_limits<float>::infinity();
+
+// traverse.hpp:70-83 — layout-identical to fkd_hit
+struct Hit {
+    std::int32_t node = -1;
+    float dist2 = kInfRadius;
+
+    float distance() const { return std::sqrt(dist2); }
+    bool operator==(const Hit&) const = default;
+};
+static_assert(sizeof(Hit) == sizeof(fkd_hit) && alignof(Hit) == alignof(fkd_hit));
+
+inline bool hit_order(const Hit& a, const Hit& b) {
+    if (a.dist2 != b.dist2) return a.dist2 < b.dist2;
+    return a.node < b.node;
+}
+
+// traverse.hpp:46-54 — layout-identical to fkd_query_stats
+struct QueryStats {
+    long long steps = 0;
+    long long nodes_visited = 0;
+    long long nodes_processed = 0;
+    static constexpr int state_node_ids = 2;
+};
+static_assert(sizeof(QueryStats) == sizeof(fkd_query_stats));
+
+enum class Engine { stack_free, recursive };  // batch.hpp:10
+enum class QueryKind { fcp, knn };            // batch.hpp:11
+
+// point.hpp:14-50 (the parts the query path uses)
+class PointSet {
+public:
+    PointSet() = default;
+    explicit PointSet(int dim) : dim_(dim) {
+        if (dim < 0) throw DataError("point set: negative dimension");
+    }
+    PointSet(int dim, std::vector<float> data) : dim_(dim), data_(std::move(data)) {
+        if (dim < 0) throw DataError("point set: negative dimension");
+        if (dim == 0 && !data_.empty()) throw DataError("point set: data with zero dimension");
+        if (dim > 0 && data_.size() % static_cast<std::size_t>(dim) != 0)
+            throw DataError("point set: data size is not a multiple of the dimension");
+    }
+    int dim() const { return dim_; }
+    int size() const { return dim_ == 0 ? 0 : static_cast<int>(data_.size() / static_cast<std::size_t>(dim_)); }
+    bool empty() const { return data_.empty(); }
+    std::span<const float> operator[](int i) const {
+        return {data_.data() + static_cast<std::size_t>(i) * dim_, static_cast<std::size_t>(dim_)};
+    }
+    const std::vector<float>& raw() const { return data_; }
+    std::vector<float>& raw() { return data_; }
+
+private:
+    int dim_ = 0;
+    std::vector<float> data_;
+};
+
+// batch.hpp:16-23 (+ B200 switches)
+struct BatchOptions {
+    QueryKind kind = QueryKind::fcp;
+    int k = 1;
+    float max_radius = kInfRadius;
+    Engine engine = Engine::stack_free;
+    int threads = 0;  // accepted for signature parity; ignored on the GPU
+    bool collect_stats = false;
+    bool morton = true;      // walk in Morton order; results stay in input order
+    bool unordered = false;  // left-first child order
+
+    fkd_batch_options to_c() const {
+        fkd_batch_options o;
+        fkd_default_options(&o);
+        o.kind = kind == QueryKind::knn ? FKD_KNN : FKD_FCP;
+        o.k = k;
+        o.max_radius = max_radius;
+        o.engine = engine == Engine::recursive ? FKD_ENGINE_RECURSIVE : FKD_ENGINE_STACK_FREE;
+        o.threads = threads;
+        o.collect_stats = collect_stats ? 1 : 0;
+        o.flags = (morton ? FKD_FLAG_MORTON : FKD_FLAG_NO_MORTON) | (unordered ? FKD_FLAG_UNORDERED : 0u);
+        return o;
+    }
+};
+
+// batch.hpp:27-41
+struct BatchResult {
+    int stride = 1;
+    std::vector<std::int32_t> counts;
+    std::vector<Hit> hits;
+    QueryStats stats;
+
+    std::span<const Hit> hits_for(int query) const {
+        return {hits.data() + static_cast<std::size_t>(query) * stride,
+                static_cast<std::size_t>(counts[static_cast<std::size_t>(query)])};
+    }
+    std::uint64_t result_hash() const {
+        return fkd_result_hash(counts.data(), reinterpret_cast<const fkd_hit*>(hits.data()),
+                               static_cast<int64_t>(counts.size()), stride);
+    }
+};
+
+// tree.hpp:41-65: a device-resident level-order tree (round-robin split).
+class KdTree {
+public:
+    KdTree() = default;
+
+    static KdTree from_level_order(const PointSet& nodes, std::span<const int> devices = {}) {
+        return from_level_order(nodes.raw().data(), nodes.size(), nodes.dim(), devices);
+    }
+
+    static KdTree from_level_order(const float* level_order, long long n, int dim,
+                                   std::span<const int> devices = {}) {
+        fkd_tree* h = nullptr;
+        std::vector<int32_t> devs(devices.begin(), devices.end());
+        check(fkd_tree_create(level_order, n, dim, devs.empty() ? nullptr : devs.data(),
+                              static_cast<int32_t>(devs.size()), &h));
+        return adopt(h);
+    }
+
+    // Takes ownership of a handle from fkd_tree_create / fkd_tree_create_device.
+    static KdTree adopt(fkd_tree* h) {
+        KdTree t;
+        t.h_ = std::shared_ptr<fkd_tree>(h, fkd_tree_destroy);
+        return t;
+    }
+
+    int size() const { return h_ ? static_cast<int>(fkd_tree_size(h_.get())) : 0; }
+    int dim() const { return h_ ? fkd_tree_dim(h_.get()) : 0; }
+    bool empty() const { return size() == 0; }
+    const fkd_tree* handle() const { return h_.get(); }
+
+private:
+    std::shared_ptr<fkd_tree> h_;
+};
+
+// tree.cpp:80-89: host build of the unique left-balanced tree, then upload.
+inline PointSet build_level_order(const PointSet& points) {
+    std::vector<float> out(points.raw().size());
+    check(fkd_build_tree(points.raw().data(), points.size(), points.dim(), out.data()));
+    return PointSet(points.dim(), std::move(out));
+}
+
+inline KdTree build_tree(const PointSet& points, std::span<const int> devices = {}) {
+    return KdTree::from_level_order(build_level_order(points), devices);
+}
+
+// batch.cpp:71-134
+inline BatchResult run_batch(const KdTree& tree, const float* queries, long long m, int dim,
+                             const BatchOptions& options) {
+    if (options.kind == QueryKind::knn && options.k < 1)
+        throw std::invalid_argument("knn: k must be >= 1");
+    BatchResult res;
+    res.stride = options.kind == QueryKind::knn ? options.k : 1;
+    res.counts.resize(static_cast<std::size_t>(m));
+    res.hits.resize(static_cast<std::size_t>(m) * res.stride);
+    const fkd_batch_options o = options.to_c();
+    fkd_query_stats st{0, 0, 0};
+    check(fkd_run_batch(tree.handle(), queries, m, dim, &o, res.counts.data(),
+                        reinterpret_cast<fkd_hit*>(res.hits.data()), &st));
+    if (options.collect_stats) res.stats = QueryStats{st.steps, st.nodes_visited, st.nodes_processed};
+    return res;
+}
+
+inline BatchResult run_batch(const KdTree& tree, const PointSet& queries, const BatchOptions& options) {
+    return run_batch(tree, queries.raw().data(), queries.size(), queries.dim(), options);
+}
+
+// traverse.cpp:25-39 over runtime-dimension spans
+inline std::optional<Hit> fcp(const KdTree& tree, std::span<const float> query,
+                              float max_radius = kInfRadius, QueryStats* stats = nullptr) {
+    Hit h;
+    int32_t count = 0;
+    fkd_query_stats st{0, 0, 0};
+    check(fkd_fcp(tree.handle(), query.data(), static_cast<int32_t>(query.size()), max_radius,
+                  reinterpret_cast<fkd_hit*>(&h), &count, stats ? &st : nullptr));
+    if (stats) *stats = QueryStats{st.steps, st.nodes_visited, st.nodes_processed};
+    return count ? std::optional<Hit>(h) : std::nullopt;
+}
+
+inline std::vector<Hit> knn(const KdTree& tree, std::span<const float> query, int k,
+                            float max_radius = kInfRadius, QueryStats* stats = nullptr) {
+    std::vector<Hit> out(static_cast<std::size_t>(k > 0 ? k : 1));
+    int32_t count = 0;
+    fkd_query_stats st{0, 0, 0};
+    check(fkd_knn(tree.handle(), query.data(), static_cast<int32_t>(query.size()), k, max_radius,
+                  reinterpret_cast<fkd_hit*>(out.data()), &count, stats ? &st : nullptr));
+    if (stats) *stats = QueryStats{st.steps, st.nodes_visited, st.nodes_processed};
+    out.resize(static_cast<std::size_t>(count));
+    return out;
+}
+
+// ---- templated float point types (north_star: "fcp and kNN entry points
+// over templated float point types").  Any PointT whose coordinates are D
+// contiguous floats (float2/float3/float4, std::array<float, D>, a POD
+// struct of D floats) dispatches straight to the D-specialised kernels.
+template <class PointT>
+constexpr int point_dim_v = static_cast<int>(sizeof(PointT) / sizeof(float));
+
+template <class PointT>
+inline std::optional<Hit> fcp(const KdTree& tree, const PointT& q, float max_radius = kInfRadius) {
+    static_assert(sizeof(PointT) % sizeof(float) == 0, "PointT must be a packed float vector");
+    return fcp(tree, std::span<const float>(reinterpret_cast<const float*>(&q), point_dim_v<PointT>),
+               max_radius);
+}
+
+template <class PointT>
+inline std::vector<Hit> knn(const KdTree& tree, const PointT& q, int k, float max_radius = kInfRadius) {
+    static_assert(sizeof(PointT) % sizeof(float) == 0, "PointT must be a packed float vector");
+    return knn(tree, std::span<const float>(reinterpret_cast<const float*>(&q), point_dim_v<PointT>), k,
+               max_radius);
+}
+
+// Batches of typed points: contiguous PointT[m].
+template <class PointT>
+inline BatchResult run_batch(const KdTree& tree, std::span<const PointT> queries, const BatchOptions& options) {
+    static_assert(sizeof(PointT) % sizeof(float) == 0, "PointT must be a packed float vector");
+    return run_batch(tree, reinterpret_cast<const float*>(queries.data()),
+                     static_cast<long long>(queries.size()), point_dim_v<PointT>, options);
+}
+
+template <class PointT>
+inline KdTree tree_from_level_order(std::span<const PointT> nodes, std::span<const int> devices = {}) {
+    return KdTree::from_level_order(reinterpret_cast<const float*>(nodes.data()),
+                                    static_cast<long long>(nodes.size()), point_dim_v<PointT>, devices);
+}
+
+}  // namespace flatkd::b200

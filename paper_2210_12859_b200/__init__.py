@@ -1,0 +1,360 @@
+"""B200-native stack-free k-d tree queries (arXiv 2210.12859), Python face.
+
+A thin ctypes mirror of the reference's C++ query API
+(``/root/reference/proj/include/flatkd/{batch,traverse,tree,point}.hpp``)
+over the C ABI in ``include/fkd_b200.h``.  Every query is answered by the
+sm_100a kernels in ``libfkd_b200.so``; there is no CPU fallback — without
+the library this package raises on import, and without a GPU the query
+entry points raise :class:`DeviceError`.
+
+Reference mapping:
+
+=============================  ===========================================
+reference                      here
+=============================  ===========================================
+``flatkd::run_batch``          :func:`run_batch`     (batch.cpp:71-134)
+``flatkd::fcp`` / ``knn``      :func:`fcp` / :func:`knn` (traverse.cpp:25-39)
+``KdTree::from_level_order``   :meth:`KdTree.from_level_order` (tree.cpp:71-78)
+``flatkd::build_tree``         :func:`build_tree`    (tree.cpp:80-89)
+``BatchOptions``               :class:`BatchOptions` (batch.hpp:16-23)
+``BatchResult``                :class:`BatchResult`  (batch.hpp:27-41)
+``Hit`` / ``QueryStats``       :data:`HIT_DTYPE` / :class:`QueryStats`
+``write_query_results``        :func:`write_query_results` (batch.cpp:136-158)
+``random_points``              :func:`random_points` (rng.hpp:46-53)
+``DataError``                  :class:`DataError`    (error.hpp:9-12)
+``std::invalid_argument``      :class:`InvalidArgument` (a ``ValueError``)
+=============================  ===========================================
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import math
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from ._lib import LIB, LIB_PATH, fkd_batch_options, fkd_query_stats, fkd_timings
+
+__all__ = [
+    "BatchOptions", "BatchResult", "DataError", "DeviceError", "Engine", "HIT_DTYPE",
+    "InvalidArgument", "InvariantError", "KdTree", "QueryKind", "QueryStats", "build_tree",
+    "clustered_points", "fcp", "knn", "random_points", "result_hash", "run_batch",
+    "run_batch_device", "write_query_results", "LIB_PATH",
+]
+
+HIT_DTYPE = np.dtype([("node", "<i4"), ("dist2", "<f4")])  # flatkd::Hit, 8 bytes
+INF = float("inf")
+
+FLAG_MORTON = 0x1
+FLAG_UNORDERED = 0x2
+FLAG_NO_MORTON = 0x4
+
+
+class DataError(RuntimeError):
+    """flatkd::DataError — bad or inconsistent input (error.hpp:9-12)."""
+
+
+class InvariantError(RuntimeError):
+    """flatkd::InvariantError (error.hpp:15-18)."""
+
+
+class InvalidArgument(ValueError):
+    """std::invalid_argument (e.g. knn k < 1, batch.cpp:72-73)."""
+
+
+class DeviceError(RuntimeError):
+    """CUDA failure or no usable B200 — there is no CPU fallback."""
+
+
+_STATUS = {1: InvalidArgument, 2: DataError, 3: InvariantError, 4: DeviceError, 5: DeviceError}
+
+
+def _check(rc: int) -> None:
+    if rc != 0:
+        msg = LIB.fkd_last_error().decode()
+        raise _STATUS.get(rc, DeviceError)(msg)
+
+
+class QueryKind(enum.IntEnum):
+    fcp = 0
+    knn = 1
+
+
+class Engine(enum.IntEnum):
+    stack_free = 0
+    recursive = 1
+
+
+@dataclass
+class BatchOptions:
+    """flatkd::BatchOptions (batch.hpp:16-23) + B200 switches."""
+
+    kind: QueryKind = QueryKind.fcp
+    k: int = 1
+    max_radius: float = INF
+    engine: Engine = Engine.stack_free
+    threads: int = 0            # accepted, ignored on the GPU
+    collect_stats: bool = False
+    morton: bool = True         # walk in Morton order (results stay in input order)
+    unordered: bool = False     # left-first child order
+
+    def to_c(self) -> fkd_batch_options:
+        o = fkd_batch_options()
+        o.kind = int(self.kind)
+        o.k = int(self.k)
+        o.max_radius = float(self.max_radius)
+        o.engine = int(self.engine)
+        o.threads = int(self.threads)
+        o.collect_stats = int(bool(self.collect_stats))
+        flags = FLAG_MORTON if self.morton else FLAG_NO_MORTON
+        if self.unordered:
+            flags |= FLAG_UNORDERED
+        o.flags = flags
+        return o
+
+    @property
+    def stride(self) -> int:
+        return int(self.k) if self.kind == QueryKind.knn else 1
+
+
+@dataclass
+class QueryStats:
+    """flatkd::QueryStats (traverse.hpp:46-54)."""
+
+    steps: int = 0
+    nodes_visited: int = 0
+    nodes_processed: int = 0
+
+    @classmethod
+    def from_c(cls, s: fkd_query_stats) -> "QueryStats":
+        return cls(int(s.steps), int(s.nodes_visited), int(s.nodes_processed))
+
+
+@dataclass
+class BatchResult:
+    """flatkd::BatchResult (batch.hpp:27-41): fixed-stride slots in input order."""
+
+    stride: int
+    counts: np.ndarray                   # int32[m]
+    hits: np.ndarray                     # HIT_DTYPE[m * stride], empty slots {-1, inf}
+    stats: QueryStats = field(default_factory=QueryStats)
+
+    def hits_for(self, query: int) -> np.ndarray:
+        base = query * self.stride
+        return self.hits[base: base + int(self.counts[query])]
+
+    def result_hash(self) -> int:
+        return result_hash(self.counts, self.hits, self.stride)
+
+
+def _f32(a, dim: Optional[int] = None) -> np.ndarray:
+    arr = np.ascontiguousarray(a, dtype=np.float32)
+    if arr.ndim == 1 and dim is not None:
+        arr = arr.reshape(-1, dim) if arr.size else arr.reshape(0, dim)
+    return arr
+
+
+class KdTree:
+    """Device-resident level-order tree (the reference's KdTree, tree.hpp:41-65,
+    round-robin split policy).  Immutable; safe to share between threads."""
+
+    def __init__(self, handle, n: int, dim: int, nodes: Optional[np.ndarray]):
+        self._h = handle
+        self._n = n
+        self._dim = dim
+        self._nodes = nodes
+
+    @classmethod
+    def from_level_order(cls, nodes, devices: Optional[Sequence[int]] = None) -> "KdTree":
+        """Adopt a level-order array without reordering it (tree.cpp:71-78)."""
+        arr = _f32(nodes)
+        if arr.ndim != 2:
+            raise DataError("point set: expected an (n, dim) array")
+        n, dim = arr.shape
+        h = C.c_void_p()
+        if devices:
+            devs = (C.c_int32 * len(devices))(*devices)
+            _check(LIB.fkd_tree_create(arr.ctypes.data, n, dim, devs, len(devices), C.byref(h)))
+        else:
+            _check(LIB.fkd_tree_create(arr.ctypes.data, n, dim, None, 0, C.byref(h)))
+        return cls(h, n, dim, arr)
+
+    @classmethod
+    def from_device(cls, tensor, stream=None) -> "KdTree":
+        """Adopt a level-order torch CUDA tensor (n, dim) float32 (copied)."""
+        if not tensor.is_cuda or tensor.dtype.itemsize != 4 or tensor.dim() != 2:
+            raise DataError("expected a CUDA float32 (n, dim) tensor")
+        t = tensor.contiguous()
+        n, dim = t.shape
+        h = C.c_void_p()
+        _check(LIB.fkd_tree_create_device(C.c_void_p(t.data_ptr()), n, dim, _stream_ptr(stream),
+                                          C.byref(h)))
+        return cls(h, n, dim, None)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            LIB.fkd_tree_destroy(h)
+            self._h = None
+
+    def size(self) -> int:
+        return self._n
+
+    def dim(self) -> int:
+        return self._dim
+
+    def empty(self) -> bool:
+        return self._n == 0
+
+    def nodes(self) -> Optional[np.ndarray]:
+        return self._nodes
+
+    @property
+    def handle(self):
+        return self._h
+
+
+def build_tree(points, devices: Optional[Sequence[int]] = None) -> KdTree:
+    """flatkd::build_tree (tree.cpp:80-89) + upload: the unique left-balanced tree."""
+    return KdTree.from_level_order(build_level_order(points), devices)
+
+
+def build_level_order(points) -> np.ndarray:
+    """Host builder only: the reference's level-order array (byte-identical)."""
+    arr = _f32(points)
+    if arr.ndim != 2:
+        raise DataError("point set: expected an (n, dim) array")
+    out = np.empty_like(arr)
+    _check(LIB.fkd_build_tree(arr.ctypes.data, arr.shape[0], arr.shape[1], out.ctypes.data))
+    return out
+
+
+def run_batch(tree: KdTree, queries, options: Optional[BatchOptions] = None) -> BatchResult:
+    """flatkd::run_batch (batch.cpp:71-134) on the GPU, host buffers in and out."""
+    options = options or BatchOptions()
+    q = _f32(queries, tree.dim())
+    if q.ndim != 2:
+        raise DataError("queries: expected an (m, dim) array")
+    m, dim = q.shape
+    if options.kind == QueryKind.knn and options.k < 1:
+        raise InvalidArgument("knn: k must be >= 1")
+    stride = options.stride
+    counts = np.zeros(m, np.int32)
+    hits = np.empty(m * stride, HIT_DTYPE)
+    st = fkd_query_stats()
+    o = options.to_c()
+    _check(LIB.fkd_run_batch(tree.handle, q.ctypes.data, m, dim, C.byref(o), counts.ctypes.data,
+                             hits.ctypes.data, C.byref(st)))
+    return BatchResult(stride, counts, hits, QueryStats.from_c(st) if options.collect_stats else QueryStats())
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        return None
+    if hasattr(stream, "cuda_stream"):
+        return C.c_void_p(stream.cuda_stream)
+    return C.c_void_p(int(stream))
+
+
+def run_batch_device(tree: KdTree, queries, counts, hits, options: Optional[BatchOptions] = None,
+                     stream=None, per_query=None, timings: bool = False):
+    """Device-resident batch: torch CUDA tensors in and out, launched on `stream`
+    (default: torch's current stream).  Returns (QueryStats, timings dict|None)."""
+    import torch
+
+    options = options or BatchOptions()
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    m = queries.shape[0]
+    dim = queries.shape[1] if queries.dim() == 2 else tree.dim()
+    st = fkd_query_stats()
+    tm = fkd_timings()
+    o = options.to_c()
+    _check(LIB.fkd_run_batch_device(
+        tree.handle, C.c_void_p(queries.data_ptr()), m, dim, C.byref(o),
+        C.c_void_p(counts.data_ptr()), C.c_void_p(hits.data_ptr()),
+        C.byref(st) if options.collect_stats else None,
+        C.c_void_p(per_query.data_ptr()) if per_query is not None else None,
+        _stream_ptr(stream), C.byref(tm) if timings else None))
+    tdict = None
+    if timings:
+        tdict = {"order_ms": tm.order_ms, "walk_ms": tm.walk_ms, "launches": tm.launches,
+                 "walk_launches": tm.walk_launches}
+    return QueryStats.from_c(st), tdict
+
+
+def fcp(tree: KdTree, query, max_radius: float = INF, stats: bool = False):
+    """Closest stored point within max_radius (inclusive), or None (traverse.cpp:25-30).
+    Returns (node, dist2) or None; with stats=True returns (hit, QueryStats)."""
+    q = _f32(query).reshape(-1)
+    out = np.empty(1, HIT_DTYPE)
+    cnt = C.c_int32(0)
+    st = fkd_query_stats()
+    _check(LIB.fkd_fcp(tree.handle, q.ctypes.data, len(q), C.c_float(max_radius), out.ctypes.data,
+                       C.byref(cnt), C.byref(st) if stats else None))
+    hit = (int(out[0]["node"]), float(out[0]["dist2"])) if cnt.value else None
+    return (hit, QueryStats.from_c(st)) if stats else hit
+
+
+def knn(tree: KdTree, query, k: int, max_radius: float = INF, stats: bool = False):
+    """Up to k nearest within max_radius, ascending by (dist2, node) (traverse.cpp:32-39)."""
+    q = _f32(query).reshape(-1)
+    out = np.empty(max(int(k), 1), HIT_DTYPE)
+    cnt = C.c_int32(0)
+    st = fkd_query_stats()
+    _check(LIB.fkd_knn(tree.handle, q.ctypes.data, len(q), int(k), C.c_float(max_radius),
+                       out.ctypes.data, C.byref(cnt), C.byref(st) if stats else None))
+    hits = [(int(h["node"]), float(h["dist2"])) for h in out[: cnt.value]]
+    return (hits, QueryStats.from_c(st)) if stats else hits
+
+
+def result_hash(counts, hits, stride: int) -> int:
+    """BatchResult::result_hash (batch.cpp:30-48)."""
+    c = np.ascontiguousarray(counts, np.int32)
+    h = np.ascontiguousarray(hits, HIT_DTYPE)
+    return int(LIB.fkd_result_hash(c.ctypes.data, h.ctypes.data, len(c), int(stride)))
+
+
+def _format_float(v: np.float32) -> str:
+    # io::format_float: "%.9g" (io.cpp:163-167); sqrt in float (traverse.hpp:74)
+    f = float(v)
+    if math.isinf(f):
+        return "inf" if f > 0 else "-inf"
+    if math.isnan(f):
+        return "nan"
+    return "%.9g" % f
+
+
+def write_query_results(result: BatchResult) -> str:
+    """Text form of write_query_results (batch.cpp:136-158)."""
+    lines = []
+    for qi in range(len(result.counts)):
+        hs = result.hits_for(qi)
+        dist = np.sqrt(hs["dist2"].astype(np.float32))
+        if result.stride == 1:
+            lines.append("-1,inf" if len(hs) == 0 else f"{int(hs[0]['node'])},{_format_float(dist[0])}")
+        else:
+            parts = [str(len(hs))]
+            for h, d in zip(hs, dist):
+                parts.append(str(int(h["node"])))
+                parts.append(_format_float(d))
+            lines.append(",".join(parts))
+    return "".join(line + "\n" for line in lines)
+
+
+def random_points(seed: int, stream: int, count: int, dim: int) -> np.ndarray:
+    """random_points(derive_stream_seed(seed, stream), count, dim) (rng.hpp:26-53)."""
+    out = np.empty(count * dim, np.float32)
+    _check(LIB.fkd_random_points(seed, stream, count, dim, out.ctypes.data))
+    return out.reshape(count, dim)
+
+
+def clustered_points(seed: int, stream: int, count: int, dim: int, blobs: int = 64,
+                     sigma: float = 0.02) -> np.ndarray:
+    """Gaussian blobs (SURVEY §8(d) C3 workload; no reference counterpart)."""
+    out = np.empty(count * dim, np.float32)
+    _check(LIB.fkd_clustered_points(seed, stream, count, dim, blobs, C.c_float(sigma),
+                                    out.ctypes.data))
+    return out.reshape(count, dim)

@@ -1,0 +1,717 @@
+// capi.cu — the C ABI (include/fkd_b200.h): device tree store, batch
+// dispatch, validation and the chunked host pipeline.
+//
+// Replaces flatkd::run_batch (src/batch.cpp:71-134) and
+// KdTree::from_level_order (src/tree.cpp:71-78) at the drop-in boundary.
+// No CPU fallback exists: every query is answered by the sm_100a kernels in
+// walk.cuh; without a usable device the calls fail with FKD_NO_DEVICE.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "fkd_b200.h"
+#include "order.cuh"
+#include "walk.cuh"
+#include "walk_inst.cuh"
+
+namespace fkd {
+namespace {
+
+thread_local std::string g_err;
+
+fkd_status fail(fkd_status s, const std::string& msg) {
+    g_err = msg;
+    return s;
+}
+
+#define FKD_CUDA(expr)                                                                        \
+    do {                                                                                      \
+        cudaError_t e_ = (expr);                                                              \
+        if (e_ != cudaSuccess)                                                                \
+            return fail(FKD_CUDA_ERROR, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+constexpr int64_t kSortChunk = int64_t(1) << 30;  // u32 ids, int item counts in CUB
+
+// Store layout: padded vectors (1, 2, 4, 4, 8, 8, 8, 8 floats) by default;
+// FKD_LAYOUT=packed keeps 3-D nodes at 12 bytes (chosen
+// by measurement).
+int store_stride(int dim) {
+    static const bool packed = [] {
+        const char* e = std::getenv("FKD_LAYOUT");
+        return e && std::strcmp(e, "packed") == 0;
+    }();
+    switch (dim) {
+        case 1: return 1;
+        case 2: return 2;
+        case 3: return packed ? 3 : 4;
+        case 4: return 4;
+        case 5: case 6: case 7: case 8: return 8;
+        default: return dim;
+    }
+}
+
+struct Workspace {
+    int device = 0;
+    cudaStream_t stream = nullptr;  // own stream (host path)
+    cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+    uint32_t* keys = nullptr;       // [2 * cap] keys in/out
+    uint32_t* ids = nullptr;        // [2 * cap] ids in/out
+    int64_t key_cap = 0;
+    void* sort_tmp = nullptr;
+    size_t sort_tmp_bytes = 0;
+    unsigned long long* small = nullptr;    // [4]: bad, steps, visited, processed
+    unsigned long long* h_small = nullptr;  // pinned mirror
+    // host-path staging
+    float* q = nullptr;
+    int64_t q_cap = 0;
+    int32_t* counts = nullptr;
+    int64_t c_cap = 0;
+    fkd_hit* hits = nullptr;
+    int64_t h_cap = 0;
+
+    ~Workspace() {
+        cudaSetDevice(device);
+        cudaFree(keys);
+        cudaFree(ids);
+        cudaFree(sort_tmp);
+        cudaFree(small);
+        cudaFreeHost(h_small);
+        cudaFree(q);
+        cudaFree(counts);
+        cudaFree(hits);
+        for (auto& e : ev)
+            if (e) cudaEventDestroy(e);
+        if (stream) cudaStreamDestroy(stream);
+    }
+};
+
+template <class T>
+cudaError_t grow(T*& p, int64_t& cap, int64_t need) {
+    if (need <= cap) return cudaSuccess;
+    cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    const int64_t want = std::max<int64_t>(need, 1024);
+    cudaError_t e = cudaMalloc(&p, size_t(want) * sizeof(T));
+    if (e == cudaSuccess) cap = want;
+    return e;
+}
+
+struct Replica {
+    int device = 0;
+    float* nodes = nullptr;  // n x stride
+    std::mutex mu;
+    std::vector<Workspace*> pool;
+
+    ~Replica() {
+        for (Workspace* w : pool) delete w;
+        cudaSetDevice(device);
+        cudaFree(nodes);
+    }
+};
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+}  // namespace
+
+const char* set_host_error(const std::string& msg) {
+    g_err = msg;
+    return g_err.c_str();
+}
+
+}  // namespace fkd
+
+struct fkd_tree {
+    int64_t n = 0;
+    int32_t dim = 0;
+    int32_t stride = 0;
+    fkd::MortonFrame frame{};
+    std::vector<fkd::Replica*> reps;
+};
+
+namespace fkd {
+namespace {
+
+fkd_status acquire_ws(Replica& r, Workspace** out) {
+    {
+        std::lock_guard<std::mutex> lk(r.mu);
+        if (!r.pool.empty()) {
+            *out = r.pool.back();
+            r.pool.pop_back();
+            return FKD_OK;
+        }
+    }
+    auto* w = new Workspace();
+    w->device = r.device;
+    DeviceGuard g(r.device);
+    cudaError_t e = cudaStreamCreateWithFlags(&w->stream, cudaStreamNonBlocking);
+    for (auto& ev : w->ev)
+        if (e == cudaSuccess) e = cudaEventCreate(&ev);
+    if (e == cudaSuccess) e = cudaMalloc(&w->small, 4 * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMallocHost(&w->h_small, 4 * sizeof(unsigned long long));
+    if (e != cudaSuccess) {
+        delete w;
+        return fail(FKD_CUDA_ERROR, std::string("workspace: ") + cudaGetErrorString(e));
+    }
+    *out = w;
+    return FKD_OK;
+}
+
+void release_ws(Replica& r, Workspace* w) {
+    std::lock_guard<std::mutex> lk(r.mu);
+    r.pool.push_back(w);
+}
+
+int walk_bucket_of(int k) {
+    if (k <= 1) return 1;
+    if (k <= 2) return 2;
+    if (k <= 4) return 4;
+    if (k <= 8) return 8;
+    if (k <= 16) return 16;
+    if (k <= 32) return 32;
+    if (k <= 64) return 64;
+    return 0;
+}
+
+// Validation of batch.cpp:72-80, in the reference's order.
+fkd_status validate(const fkd_tree* t, int64_t m, int32_t dim, const fkd_batch_options* o,
+                    float* cap2) {
+    if (!t) return fail(FKD_INVALID_ARGUMENT, "null tree");
+    if (!o) return fail(FKD_INVALID_ARGUMENT, "null options");
+    if (o->kind != FKD_FCP && o->kind != FKD_KNN)
+        return fail(FKD_INVALID_ARGUMENT, "unknown query kind");
+    if (o->kind == FKD_KNN && o->k < 1) return fail(FKD_INVALID_ARGUMENT, "knn: k must be >= 1");
+    if (std::isnan(o->max_radius) || o->max_radius < 0.0f)
+        return fail(FKD_DATA_ERROR, "max radius must be >= 0 or inf");
+    if (o->engine != FKD_ENGINE_STACK_FREE && o->engine != FKD_ENGINE_RECURSIVE)
+        return fail(FKD_INVALID_ARGUMENT, "unknown engine");
+    if (m < 0) return fail(FKD_INVALID_ARGUMENT, "negative query count");
+    if (t->n > 0 && m > 0 && dim != t->dim)
+        return fail(FKD_DATA_ERROR, "query dimension " + std::to_string(dim) +
+                                        " does not match tree dimension " + std::to_string(t->dim));
+    if (dim < 1 && m > 0) return fail(FKD_DATA_ERROR, "query dimension must be >= 1");
+    *cap2 = o->max_radius * o->max_radius;  // squared_radius_cap (point.hpp:78-82)
+    return FKD_OK;
+}
+
+bool use_morton(const fkd_tree* t, const fkd_batch_options* o, int64_t m) {
+    if (o->flags & FKD_FLAG_NO_MORTON) return false;
+    if (!(o->flags & FKD_FLAG_MORTON)) return false;
+    return t->n > 0 && m > 1 && t->dim <= 8;
+}
+
+// Enqueues one batch (device pointers) on `st`; no synchronisation.  Writes
+// the first bad query id and the stat totals into w->small.
+fkd_status enqueue(const fkd_tree* t, Replica& r, Workspace* w, const float* d_q, int64_t m,
+                   const fkd_batch_options* o, float cap2, int32_t* d_counts, fkd_hit* d_hits,
+                   fkd_query_stats* d_per_query, bool stats, cudaStream_t st, int* launches,
+                   int* walk_launches, cudaEvent_t ev_mid) {
+    const int k = o->kind == FKD_KNN ? o->k : 1;
+    if (t->n == 0) {  // every query returns empty; queries are not read (batch.cpp:75)
+        *launches += fill_empty(d_counts, d_hits, m, k, st);
+        FKD_CUDA(cudaGetLastError());
+        return FKD_OK;
+    }
+    const bool sort = use_morton(t, o, m);
+    const int64_t chunk = sort ? std::min<int64_t>(m, kSortChunk) : m;
+    if (sort) {
+        if (2 * chunk > w->key_cap) {
+            cudaFree(w->keys);
+            cudaFree(w->ids);
+            w->keys = w->ids = nullptr;
+            w->key_cap = 0;
+            FKD_CUDA(cudaMalloc(&w->keys, size_t(2 * chunk) * sizeof(uint32_t)));
+            FKD_CUDA(cudaMalloc(&w->ids, size_t(2 * chunk) * sizeof(uint32_t)));
+            w->key_cap = 2 * chunk;
+        }
+        const size_t need = morton_temp_bytes(chunk);
+        if (need > w->sort_tmp_bytes) {
+            cudaFree(w->sort_tmp);
+            w->sort_tmp = nullptr;
+            w->sort_tmp_bytes = 0;
+            FKD_CUDA(cudaMalloc(&w->sort_tmp, need));
+            w->sort_tmp_bytes = need;
+        }
+    }
+    for (int64_t base = 0; base < m; base += chunk) {
+        const int64_t cm = std::min(chunk, m - base);
+        WalkArgs a{};
+        a.nodes = r.nodes;
+        a.n = int32_t(t->n);
+        a.dim = t->dim;
+        a.stride = t->stride;
+        a.queries = d_q + base * t->dim;
+        a.m = cm;
+        a.cap2 = cap2;
+        a.k = k;
+        a.recursive_stats = o->engine == FKD_ENGINE_RECURSIVE;
+        a.counts = d_counts + base;
+        a.hits = d_hits + base * k;
+        a.totals = w->small + 1;
+        a.per_query = d_per_query ? d_per_query + base : nullptr;
+        a.bad = w->small;
+        a.id_base = base;
+        if (sort) {
+            const int64_t half = w->key_cap / 2;
+            const int rc = morton_order(a.queries, cm, t->dim, t->frame, w->keys, w->keys + half,
+                                        w->ids, w->ids + half, w->sort_tmp, w->sort_tmp_bytes, st);
+            if (rc < 0) return fail(FKD_CUDA_ERROR, "morton ordering failed");
+            *launches += rc;
+            a.order = w->ids + half;
+        }
+        if (ev_mid && base == 0) FKD_CUDA(cudaEventRecord(ev_mid, st));
+        const int nl = launch_walk(a, t->dim, t->stride, stats, (o->flags & FKD_FLAG_UNORDERED) != 0, st);
+        if (nl <= 0) return fail(FKD_CUDA_ERROR, "no kernel for this configuration");
+        *launches += nl;
+        *walk_launches += nl;
+        FKD_CUDA(cudaGetLastError());
+    }
+    return FKD_OK;
+}
+
+}  // namespace
+
+int walk_bucket(int k) { return walk_bucket_of(k); }
+
+int launch_walk(const WalkArgs& a, int dim, int stride, bool stats, bool unordered,
+                cudaStream_t st) {
+    const int KB = walk_bucket_of(a.k);
+    if (KB == 0 || dim > 8) return launch_walk_heap(a, dim, stats, unordered, st);
+    switch (dim) {
+        case 1: return launch_walk_d1(a, stride, KB, stats, unordered, st);
+        case 2: return launch_walk_d2(a, stride, KB, stats, unordered, st);
+        case 3: return launch_walk_d3(a, stride, KB, stats, unordered, st);
+        case 4: return launch_walk_d4(a, stride, KB, stats, unordered, st);
+        case 5: return launch_walk_d5(a, stride, KB, stats, unordered, st);
+        case 6: return launch_walk_d6(a, stride, KB, stats, unordered, st);
+        case 7: return launch_walk_d7(a, stride, KB, stats, unordered, st);
+        case 8: return launch_walk_d8(a, stride, KB, stats, unordered, st);
+        default: return 0;
+    }
+}
+
+}  // namespace fkd
+
+using namespace fkd;
+
+extern "C" {
+
+const char* fkd_last_error(void) { return g_err.c_str(); }
+
+const char* fkd_version(void) { return "fkd_b200 0.1 (sm_100a)"; }
+
+void fkd_default_options(fkd_batch_options* o) {
+    o->kind = FKD_FCP;
+    o->k = 1;
+    o->max_radius = INFINITY;
+    o->engine = FKD_ENGINE_STACK_FREE;
+    o->threads = 0;
+    o->collect_stats = 0;
+    o->flags = FKD_FLAG_MORTON;
+}
+
+void* fkd_host_alloc(size_t bytes) {
+    void* p = nullptr;
+    if (cudaMallocHost(&p, bytes) != cudaSuccess) return nullptr;
+    return p;
+}
+
+void fkd_host_free(void* p) { cudaFreeHost(p); }
+
+int64_t fkd_tree_size(const fkd_tree* t) { return t ? t->n : 0; }
+int32_t fkd_tree_dim(const fkd_tree* t) { return t ? t->dim : 0; }
+
+void fkd_tree_destroy(fkd_tree* t) {
+    if (!t) return;
+    for (Replica* r : t->reps) delete r;
+    delete t;
+}
+
+static fkd_status set_frame(fkd_tree* t, const float* lo, const float* hi) {
+    const int dim = t->dim;
+    t->frame.bits = morton_bits_per_dim(std::min(dim, 8));
+    const float top = float((1u << t->frame.bits) - 1u);
+    for (int d = 0; d < 8; ++d) {
+        t->frame.lo[d] = 0.0f;
+        t->frame.scale[d] = 0.0f;
+    }
+    for (int d = 0; d < dim && d < 8; ++d) {
+        t->frame.lo[d] = lo[d];
+        const double ext = double(hi[d]) - double(lo[d]);
+        t->frame.scale[d] = ext > 0.0 ? float(top / ext) : 0.0f;
+    }
+    return FKD_OK;
+}
+
+static fkd_status make_replica(fkd_tree* t, int dev, const float* src, bool src_on_device,
+                               cudaStream_t st) {
+    auto* r = new Replica();
+    r->device = dev;
+    t->reps.push_back(r);
+    DeviceGuard g(dev);
+    const int64_t n = t->n;
+    if (n == 0) return FKD_OK;
+    const size_t store_bytes = size_t(n) * t->stride * sizeof(float);
+    FKD_CUDA(cudaMalloc(&r->nodes, store_bytes));
+    if (t->stride == t->dim) {
+        FKD_CUDA(cudaMemcpyAsync(r->nodes, src, store_bytes,
+                                 src_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+    } else {
+        const float* dsrc = src;
+        float* tmp = nullptr;
+        if (!src_on_device) {
+            FKD_CUDA(cudaMalloc(&tmp, size_t(n) * t->dim * sizeof(float)));
+            FKD_CUDA(cudaMemcpyAsync(tmp, src, size_t(n) * t->dim * sizeof(float),
+                                     cudaMemcpyHostToDevice, st));
+            dsrc = tmp;
+        }
+        pack_nodes(dsrc, n, t->dim, t->stride, r->nodes, st);
+        FKD_CUDA(cudaGetLastError());
+        if (tmp) {
+            FKD_CUDA(cudaStreamSynchronize(st));
+            cudaFree(tmp);
+        }
+    }
+    FKD_CUDA(cudaStreamSynchronize(st));
+    return FKD_OK;
+}
+
+fkd_status fkd_tree_create(const float* level_order, int64_t n, int32_t dim,
+                           const int32_t* devices, int32_t ndev, fkd_tree** out) {
+    if (!out) return fail(FKD_INVALID_ARGUMENT, "null output");
+    *out = nullptr;
+    if (n < 0 || n > int64_t(0x7fffffff)) return fail(FKD_DATA_ERROR, "tree size out of range");
+    if (dim < 0 || (n > 0 && dim < 1)) return fail(FKD_DATA_ERROR, "point set: negative dimension");
+    if (n > 0 && !level_order) return fail(FKD_INVALID_ARGUMENT, "null tree data");
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+        return fail(FKD_NO_DEVICE, "no CUDA device visible (the B200 path has no CPU fallback)");
+    // KdTree::from_level_order -> require_finite(nodes, "tree nodes") (tree.cpp:72)
+    std::vector<float> lo(std::max(dim, 1), INFINITY), hi(std::max(dim, 1), -INFINITY);
+    for (int64_t i = 0; i < n; ++i) {
+        const float* p = level_order + i * dim;
+        for (int d = 0; d < dim; ++d) {
+            if (!std::isfinite(p[d]))
+                return fail(FKD_DATA_ERROR, "tree nodes: non-finite coordinate in point " + std::to_string(i));
+            lo[d] = std::min(lo[d], p[d]);
+            hi[d] = std::max(hi[d], p[d]);
+        }
+    }
+    auto* t = new fkd_tree();
+    t->n = n;
+    t->dim = dim;
+    t->stride = store_stride(dim);
+    if (n > 0) set_frame(t, lo.data(), hi.data());
+    std::vector<int> devs;
+    if (devices && ndev > 0) {
+        devs.assign(devices, devices + ndev);
+    } else {
+        int cur = 0;
+        cudaGetDevice(&cur);
+        devs.push_back(cur);
+    }
+    for (int dev : devs) {
+        if (dev < 0 || dev >= count) {
+            fkd_tree_destroy(t);
+            return fail(FKD_INVALID_ARGUMENT, "device id out of range");
+        }
+        fkd_status s = make_replica(t, dev, level_order, false, nullptr);
+        if (s != FKD_OK) {
+            fkd_tree_destroy(t);
+            return s;
+        }
+    }
+    *out = t;
+    return FKD_OK;
+}
+
+fkd_status fkd_tree_create_device(const float* d_level_order, int64_t n, int32_t dim, void* stream,
+                                  fkd_tree** out) {
+    if (!out) return fail(FKD_INVALID_ARGUMENT, "null output");
+    *out = nullptr;
+    if (n < 0 || n > int64_t(0x7fffffff)) return fail(FKD_DATA_ERROR, "tree size out of range");
+    if (dim < 0 || (n > 0 && dim < 1)) return fail(FKD_DATA_ERROR, "point set: negative dimension");
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+        return fail(FKD_NO_DEVICE, "no CUDA device visible (the B200 path has no CPU fallback)");
+    int dev = 0;
+    FKD_CUDA(cudaGetDevice(&dev));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    auto* t = new fkd_tree();
+    t->n = n;
+    t->dim = dim;
+    t->stride = store_stride(dim);
+    if (n > 0) {
+        unsigned* d_lohi = nullptr;
+        unsigned long long* d_bad = nullptr;
+        std::vector<unsigned> lohi(16);
+        for (int d = 0; d < 8; ++d) {
+            lohi[2 * d] = 0xffffffffu;
+            lohi[2 * d + 1] = 0u;
+        }
+        unsigned long long bad = kNoBad;
+        cudaError_t e = cudaMalloc(&d_lohi, 16 * sizeof(unsigned));
+        if (e == cudaSuccess) e = cudaMalloc(&d_bad, sizeof(unsigned long long));
+        if (e == cudaSuccess) e = cudaMemcpyAsync(d_lohi, lohi.data(), 16 * sizeof(unsigned), cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(d_bad, &bad, sizeof(bad), cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess) {
+            tree_scan(d_level_order, n, dim, d_lohi, d_bad, st);
+            e = cudaGetLastError();
+        }
+        if (e == cudaSuccess) e = cudaMemcpyAsync(lohi.data(), d_lohi, 16 * sizeof(unsigned), cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(&bad, d_bad, sizeof(bad), cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        cudaFree(d_lohi);
+        cudaFree(d_bad);
+        if (e != cudaSuccess) {
+            delete t;
+            return fail(FKD_CUDA_ERROR, std::string("tree scan: ") + cudaGetErrorString(e));
+        }
+        if (bad != kNoBad) {
+            delete t;
+            return fail(FKD_DATA_ERROR, "tree nodes: non-finite coordinate in point " + std::to_string(bad));
+        }
+        float lo[8], hi[8];
+        for (int d = 0; d < 8; ++d) {
+            lo[d] = ordered_to_float(lohi[2 * d]);
+            hi[d] = ordered_to_float(lohi[2 * d + 1]);
+        }
+        set_frame(t, lo, hi);
+    }
+    fkd_status s = make_replica(t, dev, d_level_order, true, st);
+    if (s != FKD_OK) {
+        fkd_tree_destroy(t);
+        return s;
+    }
+    *out = t;
+    return FKD_OK;
+}
+
+static fkd_status finish_small(Workspace* w, int64_t base, unsigned long long* bad,
+                               unsigned long long tot[3]) {
+    const unsigned long long b = w->h_small[0];
+    if (b != kNoBad && (*bad == kNoBad || b + base < *bad)) *bad = b + base;
+    tot[0] += w->h_small[1];
+    tot[1] += w->h_small[2];
+    tot[2] += w->h_small[3];
+    return FKD_OK;
+}
+
+fkd_status fkd_run_batch_device(const fkd_tree* t, const float* d_q, int64_t m, int32_t dim,
+                                const fkd_batch_options* o, int32_t* d_counts, fkd_hit* d_hits,
+                                fkd_query_stats* stats, fkd_query_stats* d_per_query, void* stream,
+                                fkd_timings* timings) {
+    float cap2 = 0.0f;
+    fkd_status s = validate(t, m, dim, o, &cap2);
+    if (s != FKD_OK) return s;
+    if (stats) *stats = fkd_query_stats{0, 0, 0};
+    if (timings) *timings = fkd_timings{0.0f, 0.0f, 0, 0};
+    if (m == 0) return FKD_OK;
+    if (t->reps.empty()) return fail(FKD_NO_DEVICE, "tree has no device replica");
+    if ((reinterpret_cast<uintptr_t>(d_hits) & 7u) != 0)
+        return fail(FKD_INVALID_ARGUMENT, "hits buffer must be 8-byte aligned");
+    Replica& r = *t->reps[0];
+    DeviceGuard g(r.device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    Workspace* w = nullptr;
+    if ((s = acquire_ws(r, &w)) != FKD_OK) return s;
+    const bool want_stats = stats != nullptr || d_per_query != nullptr;
+    const unsigned long long init[4] = {kNoBad, 0, 0, 0};
+    int launches = 0, walk_launches = 0;
+    auto body = [&]() -> fkd_status {
+        FKD_CUDA(cudaMemcpyAsync(w->small, init, sizeof(init), cudaMemcpyHostToDevice, st));
+        if (timings) FKD_CUDA(cudaEventRecord(w->ev[0], st));
+        fkd_status e = enqueue(t, r, w, d_q, m, o, cap2, d_counts, d_hits, d_per_query, want_stats,
+                               st, &launches, &walk_launches, timings ? w->ev[1] : nullptr);
+        if (e != FKD_OK) return e;
+        if (timings) FKD_CUDA(cudaEventRecord(w->ev[2], st));
+        FKD_CUDA(cudaMemcpyAsync(w->h_small, w->small, sizeof(init), cudaMemcpyDeviceToHost, st));
+        FKD_CUDA(cudaStreamSynchronize(st));
+        unsigned long long bad = kNoBad, tot[3] = {0, 0, 0};
+        finish_small(w, 0, &bad, tot);
+        if (bad != kNoBad)
+            return fail(FKD_DATA_ERROR, "queries: non-finite coordinate in point " + std::to_string(bad));
+        if (stats) *stats = fkd_query_stats{int64_t(tot[0]), int64_t(tot[1]), int64_t(tot[2])};
+        if (timings) {
+            cudaEventElapsedTime(&timings->order_ms, w->ev[0], w->ev[1]);
+            cudaEventElapsedTime(&timings->walk_ms, w->ev[1], w->ev[2]);
+            timings->launches = launches;
+            timings->walk_launches = walk_launches;
+        }
+        return FKD_OK;
+    };
+    s = body();
+    release_ws(r, w);
+    return s;
+}
+
+// Host-buffer path: shard over the tree's devices, and per device split the
+// shard into chunks that alternate between two workspaces (two streams) so
+// the H2D copy of one chunk, the walk of another and the D2H copy of a third
+// overlap.  Counts and hits land directly in the caller's buffers.
+fkd_status fkd_run_batch(const fkd_tree* t, const float* queries, int64_t m, int32_t dim,
+                         const fkd_batch_options* o, int32_t* counts, fkd_hit* hits,
+                         fkd_query_stats* stats) {
+    float cap2 = 0.0f;
+    fkd_status s = validate(t, m, dim, o, &cap2);
+    if (s != FKD_OK) return s;
+    if (stats) *stats = fkd_query_stats{0, 0, 0};
+    if (m == 0) return FKD_OK;
+    if (t->reps.empty()) return fail(FKD_NO_DEVICE, "tree has no device replica");
+    const int k = o->kind == FKD_KNN ? o->k : 1;
+    const bool want_stats = o->collect_stats != 0;
+    const int ndev = int(t->reps.size());
+    const int64_t per_dev = (m + ndev - 1) / ndev;
+    static const int64_t kChunk = [] {
+        const char* e = std::getenv("FKD_CHUNK");
+        return e ? std::max<int64_t>(1024, std::atoll(e)) : int64_t(2) << 20;
+    }();
+
+    struct Job {
+        int rep;
+        Workspace* w;
+        int64_t base, count;
+    };
+    std::vector<Job> jobs;
+    std::vector<std::vector<Workspace*>> wss(ndev);
+    fkd_status err = FKD_OK;
+    for (int di = 0; di < ndev && err == FKD_OK; ++di) {
+        const int64_t lo = std::min<int64_t>(m, di * per_dev), hi = std::min<int64_t>(m, lo + per_dev);
+        if (hi <= lo) continue;
+        const int64_t nchunks = (hi - lo + kChunk - 1) / kChunk;
+        const int nws = nchunks > 1 ? 2 : 1;
+        for (int j = 0; j < nws && err == FKD_OK; ++j) {
+            Workspace* w = nullptr;
+            err = acquire_ws(*t->reps[di], &w);
+            if (err == FKD_OK) wss[di].push_back(w);
+        }
+        for (int64_t c = 0; c < nchunks && err == FKD_OK; ++c) {
+            const int64_t b = lo + c * kChunk;
+            jobs.push_back(Job{di, wss[di][c % wss[di].size()], b, std::min(kChunk, hi - b)});
+        }
+    }
+    std::vector<unsigned long long> small(jobs.size() * 4, 0);
+    if (err == FKD_OK) {
+        // size every workspace for its largest chunk before enqueueing
+        for (int di = 0; di < ndev && err == FKD_OK; ++di) {
+            DeviceGuard g(t->reps[di]->device);
+            for (Workspace* w : wss[di]) {
+                int64_t big = 0;
+                for (const Job& j : jobs)
+                    if (j.w == w) big = std::max(big, j.count);
+                cudaError_t e = grow(w->q, w->q_cap, big * dim);
+                if (e == cudaSuccess) e = grow(w->counts, w->c_cap, big);
+                if (e == cudaSuccess) e = grow(w->hits, w->h_cap, big * k);
+                if (e != cudaSuccess) err = fail(FKD_CUDA_ERROR, std::string("staging: ") + cudaGetErrorString(e));
+            }
+        }
+    }
+    // Enqueue: H2D -> order + walk -> D2H -> small D2H, per chunk.  A
+    // workspace's stream serialises its own chunks, so buffer reuse is safe.
+    for (size_t ji = 0; ji < jobs.size() && err == FKD_OK; ++ji) {
+        const Job& j = jobs[ji];
+        Replica& r = *t->reps[j.rep];
+        DeviceGuard g(r.device);
+        Workspace* w = j.w;
+        const unsigned long long init[4] = {kNoBad, 0, 0, 0};
+        int launches = 0, wl = 0;
+        auto step = [&]() -> fkd_status {
+            FKD_CUDA(cudaMemcpyAsync(w->q, queries + j.base * dim, size_t(j.count) * dim * sizeof(float),
+                                     cudaMemcpyHostToDevice, w->stream));
+            FKD_CUDA(cudaMemcpyAsync(w->small, init, sizeof(init), cudaMemcpyHostToDevice, w->stream));
+            fkd_status e = enqueue(t, r, w, w->q, j.count, o, cap2, w->counts, w->hits, nullptr,
+                                   want_stats, w->stream, &launches, &wl, nullptr);
+            if (e != FKD_OK) return e;
+            FKD_CUDA(cudaMemcpyAsync(counts + j.base, w->counts, size_t(j.count) * sizeof(int32_t),
+                                     cudaMemcpyDeviceToHost, w->stream));
+            FKD_CUDA(cudaMemcpyAsync(hits + j.base * k, w->hits, size_t(j.count) * k * sizeof(fkd_hit),
+                                     cudaMemcpyDeviceToHost, w->stream));
+            FKD_CUDA(cudaMemcpyAsync(&small[ji * 4], w->small, sizeof(init), cudaMemcpyDeviceToHost,
+                                     w->stream));
+            return FKD_OK;
+        };
+        err = step();
+    }
+    // drain every stream even after an error, then return workspaces
+    for (int di = 0; di < ndev; ++di) {
+        DeviceGuard g(t->reps[di]->device);
+        for (Workspace* w : wss[di]) {
+            cudaError_t e = cudaStreamSynchronize(w->stream);
+            if (e != cudaSuccess && err == FKD_OK)
+                err = fail(FKD_CUDA_ERROR, std::string("stream: ") + cudaGetErrorString(e));
+            release_ws(*t->reps[di], w);
+        }
+    }
+    if (err != FKD_OK) return err;
+    unsigned long long bad = kNoBad, tot[3] = {0, 0, 0};
+    for (size_t ji = 0; ji < jobs.size(); ++ji) {
+        const unsigned long long b = small[ji * 4];
+        if (b != kNoBad) bad = std::min<unsigned long long>(bad, b + jobs[ji].base);
+        for (int c = 0; c < 3; ++c) tot[c] += small[ji * 4 + 1 + c];
+    }
+    if (bad != kNoBad)
+        return fail(FKD_DATA_ERROR, "queries: non-finite coordinate in point " + std::to_string(bad));
+    if (stats) *stats = fkd_query_stats{int64_t(tot[0]), int64_t(tot[1]), int64_t(tot[2])};
+    return FKD_OK;
+}
+
+static fkd_status single(const fkd_tree* t, const float* q, int32_t dim, int kind, int32_t k,
+                         float max_radius, fkd_hit* out, int32_t* out_count, fkd_query_stats* stats) {
+    // constructor order of FcpCandidates / KnnCandidates (traverse.hpp:88-89,
+    // 115-117): the radius is checked before k.
+    if (std::isnan(max_radius) || max_radius < 0.0f)
+        return fail(FKD_DATA_ERROR, "max radius must be >= 0 or inf");
+    if (kind == FKD_KNN && k < 1) return fail(FKD_INVALID_ARGUMENT, "knn: k must be >= 1");
+    if (!t) return fail(FKD_INVALID_ARGUMENT, "null tree");
+    if (t->n > 0) {  // validate_query (traverse.hpp:186-192)
+        if (dim != t->dim)
+            return fail(FKD_DATA_ERROR, "query dimension " + std::to_string(dim) +
+                                            " does not match tree dimension " + std::to_string(t->dim));
+        for (int d = 0; d < dim; ++d)
+            if (!std::isfinite(q[d])) return fail(FKD_DATA_ERROR, "query has a non-finite coordinate");
+    }
+    fkd_batch_options o;
+    fkd_default_options(&o);
+    o.kind = kind;
+    o.k = kind == FKD_KNN ? k : 1;
+    o.max_radius = max_radius;
+    o.collect_stats = stats != nullptr;
+    o.flags = FKD_FLAG_NO_MORTON;
+    const int stride = kind == FKD_KNN ? k : 1;
+    std::vector<fkd_hit> hits(static_cast<size_t>(stride));
+    int32_t count = 0;
+    const float dummy = 0.0f;
+    fkd_status s = fkd_run_batch(t, t->n > 0 ? q : &dummy, 1, t->n > 0 ? dim : 1, &o, &count,
+                                 hits.data(), stats);
+    if (s != FKD_OK) return s;
+    std::copy(hits.begin(), hits.begin() + count, out);
+    *out_count = count;
+    return FKD_OK;
+}
+
+fkd_status fkd_fcp(const fkd_tree* t, const float* q, int32_t dim, float max_radius, fkd_hit* out,
+                   int32_t* out_count, fkd_query_stats* stats) {
+    return single(t, q, dim, FKD_FCP, 1, max_radius, out, out_count, stats);
+}
+
+fkd_status fkd_knn(const fkd_tree* t, const float* q, int32_t dim, int32_t k, float max_radius,
+                   fkd_hit* out, int32_t* out_count, fkd_query_stats* stats) {
+    return single(t, q, dim, FKD_KNN, k, max_radius, out, out_count, stats);
+}
+
+}  // extern "C"

@@ -1,0 +1,466 @@
+// walk.cuh — sm_100a kernels for the stack-free k-d tree walk.
+//
+// One thread per query.  The per-query state is the reference's two node ids
+// plus the shrinking squared radius (TraversalState, traverse.hpp:37-44);
+// every transition follows traverse_step (traverse.hpp:198-248):
+//
+//   arrived from the parent   -> process the node, step into the close child
+//   back from the close child -> far child if sd*sd <= radius2, else parent
+//   back from the far child   -> parent
+//
+// B200-specific choices:
+//   * Bounces off empty child slots (curr >= N, traverse.hpp:206-212) are
+//     resolved in registers: the node's split plane is still live, so the
+//     "step into the empty slot, step back" pair costs no load and no loop
+//     trip.  The visit sequence, the candidate updates and (in STATS mode)
+//     the step/visit counters are exactly the reference's.
+//   * The candidate list is a register-resident ascending array of KB packed
+//     64-bit keys ((dist2_bits + 1) << 32 | node): unsigned order on the key
+//     IS hit_order (traverse.hpp:80-83), because squared distances are
+//     non-negative floats whose bit patterns sort like the values.  Insertion
+//     is a branch-free min/max bubble.  The first KB-k slots hold key 0 and
+//     never move, so one kernel serves every k <= KB.  radius2 is the kth
+//     key's distance (or the cap while fewer than k hits are held) — the
+//     reference's KnnCandidates::radius2 (traverse.hpp:135-137); fcp is KB=1
+//     (FcpCandidates, traverse.hpp:86-108).
+//   * Squared distances use __fsub_rn/__fmul_rn/__fadd_rn left to right: no
+//     FMA contraction, bit-identical to point.hpp:68-75 compiled without it.
+//   * Queries may be walked in Morton order (order[] = sorted position ->
+//     query id); results are scattered straight to the query's own slot, so
+//     no separate un-permute pass exists.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "fkd_b200.h"
+
+namespace fkd {
+
+constexpr uint64_t kEmptyKey = (uint64_t(0x7f800000u + 1u) << 32) | 0xFFFFFFFFull;
+constexpr uint64_t kNoBad = ~0ull;
+
+struct WalkArgs {
+    const float* nodes;         // device tree store, `stride` floats per node
+    int32_t n;                  // tree size
+    int32_t dim;                // runtime dim (used by the dynamic-D kernel)
+    int32_t stride;             // floats per node in the store
+    const float* queries;       // m x dim row-major (caller layout)
+    int64_t m;
+    const uint32_t* order;      // walk position -> query id, or null
+    float cap2;                 // squared_radius_cap(max_radius) (point.hpp:78-82)
+    int32_t k;                  // output stride
+    int32_t recursive_stats;    // report Engine::recursive counters
+    int32_t* counts;            // [m]
+    fkd_hit* hits;              // [m * k]
+    unsigned long long* totals; // [3] steps, visited, processed (STATS)
+    fkd_query_stats* per_query; // [m] or null (STATS)
+    unsigned long long* bad;    // min id of a non-finite query
+    int64_t id_base;            // added to query ids reported through `bad`
+};
+
+__device__ __forceinline__ uint64_t make_key(float d2, int32_t node) {
+    return (uint64_t(__float_as_uint(d2) + 1u) << 32) | uint32_t(node);
+}
+
+__device__ __forceinline__ float key_dist(uint64_t key) {
+    return __uint_as_float(uint32_t(key >> 32) - 1u);
+}
+
+__device__ __forceinline__ int32_t depth_of(int32_t node) {  // tree.hpp:20-22
+    return 31 - __clz(node + 1);
+}
+
+template <int D>
+__device__ __forceinline__ int split_dim(int32_t node) {  // tree.hpp:27-29
+    return depth_of(node) % D;
+}
+
+template <int D>
+__device__ __forceinline__ float pick(const float (&a)[D], int d) {
+    float r = a[0];
+#pragma unroll
+    for (int i = 1; i < D; ++i) r = (d == i) ? a[i] : r;
+    return r;
+}
+
+// point.hpp:68-75: acc = 0; acc += (q_i - p_i)^2 left to right.  0 + x == x
+// for the non-negative first square, so the chain starts at it.
+template <int D>
+__device__ __forceinline__ float sq_dist(const float (&q)[D], const float (&p)[D]) {
+    float d0 = __fsub_rn(q[0], p[0]);
+    float acc = __fmul_rn(d0, d0);
+#pragma unroll
+    for (int i = 1; i < D; ++i) {
+        const float di = __fsub_rn(q[i], p[i]);
+        acc = __fadd_rn(acc, __fmul_rn(di, di));
+    }
+    return acc;
+}
+
+// Full point of one node.  S is the store stride: S in {2,4,8} is a padded
+// vector layout (LDG.64 / LDG.128), S == D is packed (scalar loads).
+template <int D, int S>
+__device__ __forceinline__ void load_point(const float* __restrict__ nodes, int32_t i,
+                                           float (&p)[D]) {
+    const float* base = nodes + size_t(i) * S;
+    if constexpr (S == 4) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(base));
+        const float t[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int j = 0; j < D; ++j) p[j] = t[j];
+    } else if constexpr (S == 8) {
+        const float4 v0 = __ldg(reinterpret_cast<const float4*>(base));
+        const float4 v1 = __ldg(reinterpret_cast<const float4*>(base) + 1);
+        const float t[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+        for (int j = 0; j < D; ++j) p[j] = t[j];
+    } else if constexpr (S == 2 && D == 2) {
+        const float2 v = __ldg(reinterpret_cast<const float2*>(base));
+        p[0] = v.x;
+        p[1] = v.y;
+    } else {
+#pragma unroll
+        for (int j = 0; j < D; ++j) p[j] = __ldg(base + j);
+    }
+}
+
+template <int KB>
+__device__ __forceinline__ void list_insert(uint64_t (&L)[KB], uint64_t x) {
+#pragma unroll
+    for (int j = 0; j < KB; ++j) {
+        const uint64_t lo = L[j] < x ? L[j] : x;
+        x = L[j] < x ? x : L[j];
+        L[j] = lo;
+    }
+}
+
+template <bool STATS>
+struct Counters {
+    unsigned long long steps = 0, visited = 0, processed = 0;
+    __device__ __forceinline__ void step(int s, int v, int p) {
+        if constexpr (STATS) {
+            steps += s;
+            visited += v;
+            processed += p;
+        }
+    }
+};
+
+// Warp-aggregated totals + optional per-query record.
+template <bool STATS>
+__device__ __forceinline__ void flush_stats(const WalkArgs& a, int64_t qi, bool active,
+                                            const Counters<STATS>& c) {
+    if constexpr (STATS) {
+        unsigned long long s = c.steps, v = c.visited, p = c.processed;
+        if (a.recursive_stats) {
+            // Engine::recursive counts one step per call (traverse.hpp:265) and
+            // never revisits: steps = processed + bounces, visited = processed.
+            const unsigned long long bounces = s - v;
+            s = p + bounces;
+            v = p;
+        }
+        if (!active) s = v = p = 0;
+        if (active && a.per_query) {
+            a.per_query[qi].steps = (int64_t)s;
+            a.per_query[qi].nodes_visited = (int64_t)v;
+            a.per_query[qi].nodes_processed = (int64_t)p;
+        }
+        for (int off = 16; off > 0; off >>= 1) {
+            s += __shfl_down_sync(0xffffffffu, s, off);
+            v += __shfl_down_sync(0xffffffffu, v, off);
+            p += __shfl_down_sync(0xffffffffu, p, off);
+        }
+        if ((threadIdx.x & 31) == 0) {
+            atomicAdd(a.totals + 0, s);
+            atomicAdd(a.totals + 1, v);
+            atomicAdd(a.totals + 2, p);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Register-list walk, D in 1..8 compile-time, KB slots, k <= KB at run time.
+// ---------------------------------------------------------------------------
+template <int D, int S, int KB, bool STATS, bool UNORDERED>
+__global__ void __launch_bounds__(256) walk_kernel(const WalkArgs a) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    bool active = i < a.m;
+    int64_t qi = 0;
+    float q[D];
+    if (active) {
+        qi = a.order ? int64_t(a.order[i]) : i;
+        const float* qp = a.queries + qi * D;
+        bool finite = true;
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            q[j] = __ldg(qp + j);
+            finite &= isfinite(q[j]);
+        }
+        if (!finite) {  // batch.cpp:79 -> DataError, reported by the host
+            atomicMin(a.bad, (unsigned long long)(a.id_base + qi));
+            active = false;
+        }
+    }
+    Counters<STATS> cnt;
+    if (active) {
+        uint64_t L[KB];
+        const int dummies = KB - a.k;
+#pragma unroll
+        for (int j = 0; j < KB; ++j) L[j] = j < dummies ? 0ull : kEmptyKey;
+        const float cap2 = a.cap2;
+        const int32_t n = a.n;
+        float r2 = cap2;
+
+        int32_t curr = 0, prev = -1;
+        while (n > 0) {
+            const bool from_parent = prev < curr;
+            const int d = split_dim<D>(curr);
+            float p[D];
+            float pd;
+            if constexpr (S == D && D > 1) {
+                // packed store: the full point only on first visits
+                if (from_parent) {
+                    load_point<D, S>(a.nodes, curr, p);
+                    pd = pick(p, d);
+                } else {
+                    pd = __ldg(a.nodes + size_t(curr) * S + d);
+                }
+            } else {
+                load_point<D, S>(a.nodes, curr, p);
+                pd = pick(p, d);
+            }
+            if (from_parent) {  // traverse.hpp:217-222
+                const float d2 = sq_dist(q, p);
+                const uint64_t key = make_key(d2, curr);
+                if (d2 <= cap2 && key < L[KB - 1]) {
+                    list_insert(L, key);
+                    r2 = fminf(cap2, key_dist(L[KB - 1]));
+                }
+            }
+            cnt.step(1, 1, from_parent ? 1 : 0);
+
+            const float sd = __fsub_rn(pick(q, d), pd);                // 226
+            const int cs = sd > 0.0f;                                  // 227
+            const bool fir = __fmul_rn(sd, sd) <= r2;                  // 230
+            const int32_t parent = ((curr + 1) >> 1) - 1;              // 205
+            int32_t next;
+            if constexpr (!UNORDERED) {
+                const int32_t close = 2 * curr + 1 + cs;               // 228
+                const int32_t far = 2 * curr + 2 - cs;                 // 229
+                if (from_parent)
+                    next = close;
+                else
+                    next = (prev == close && fir) ? far : parent;
+                if (next >= n) {  // empty slot: bounce + return visit, in registers
+                    cnt.step(2, 1, 0);
+                    next = (next == close && fir) ? far : parent;
+                    if (next >= n) {
+                        cnt.step(2, 1, 0);
+                        next = parent;
+                    }
+                }
+            } else {
+                // left-first order; a child is entered iff it is on the
+                // query's side or its plane is within the radius
+                const int32_t left = 2 * curr + 1, right = 2 * curr + 2;
+                const bool enter_left = !cs || fir, enter_right = cs || fir;
+                if (from_parent)
+                    next = enter_left ? left : (enter_right ? right : parent);
+                else
+                    next = (prev == left && enter_right) ? right : parent;
+                if (next >= n) {
+                    cnt.step(2, 1, 0);
+                    next = (next == left && enter_right) ? right : parent;
+                    if (next >= n) {
+                        cnt.step(2, 1, 0);
+                        next = parent;
+                    }
+                }
+            }
+            if (next < 0) break;  // 240-244: the root stepped to -1
+            prev = curr;
+            curr = next;
+        }
+
+        // fixed-stride slot in input order (batch.cpp:104-119)
+        const int k = a.k;
+        int2* out = reinterpret_cast<int2*>(a.hits + qi * k);
+        int c = 0;
+#pragma unroll
+        for (int j = 0; j < KB; ++j) {
+            const int s = j - dummies;
+            if (s >= 0) {
+                const uint64_t key = L[j];
+                out[s] = make_int2(int32_t(uint32_t(key)), int32_t(uint32_t(key >> 32) - 1u));
+                c += uint32_t(key) != 0xFFFFFFFFu;
+            }
+        }
+        a.counts[qi] = c;
+    }
+    flush_stats<STATS>(a, qi, active, cnt);
+}
+
+// ---------------------------------------------------------------------------
+// Generic walk for large k (> register buckets) and/or runtime dim > 8.
+// The query's own output slot (k entries) holds a bounded max-heap of keys
+// during the walk — the reference's KnnCandidates layout (traverse.hpp:
+// 113-175) — and is heap-sorted in place at the end; no scratch memory.
+// D == 0 means runtime dim (queries re-read through L1).
+// ---------------------------------------------------------------------------
+template <int D>
+struct QueryRegs {
+    float v[D];
+};
+
+template <int D, bool STATS, bool UNORDERED>
+__global__ void __launch_bounds__(128) walk_heap_kernel(const WalkArgs a) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    bool active = i < a.m;
+    int64_t qi = 0;
+    const int dim = D > 0 ? D : a.dim;
+    const float* qp = nullptr;
+    if (active) {
+        qi = a.order ? int64_t(a.order[i]) : i;
+        qp = a.queries + qi * dim;
+        bool finite = true;
+        for (int j = 0; j < dim; ++j) finite &= isfinite(__ldg(qp + j));
+        if (!finite) {
+            atomicMin(a.bad, (unsigned long long)(a.id_base + qi));
+            active = false;
+        }
+    }
+    Counters<STATS> cnt;
+    if (active) {
+        const int k = a.k;
+        uint64_t* heap = reinterpret_cast<uint64_t*>(a.hits + qi * k);
+        int count = 0;
+        const float cap2 = a.cap2;
+        const int32_t n = a.n;
+        float r2 = cap2;
+        int32_t curr = 0, prev = -1;
+        while (n > 0) {
+            const bool from_parent = prev < curr;
+            const int d = depth_of(curr) % dim;
+            const float* node = a.nodes + size_t(curr) * a.stride;
+            if (from_parent) {
+                float acc = 0.0f;
+                for (int j = 0; j < dim; ++j) {
+                    const float dj = __fsub_rn(__ldg(qp + j), __ldg(node + j));
+                    acc = __fadd_rn(acc, __fmul_rn(dj, dj));
+                }
+                const uint64_t key = make_key(acc, curr);
+                if (acc <= cap2) {
+                    if (count < k) {  // push + sift up (traverse.hpp:123-126)
+                        int c = count++;
+                        while (c > 0) {
+                            const int par = (c - 1) >> 1;
+                            const uint64_t pk = heap[par];
+                            if (pk >= key) break;
+                            heap[c] = pk;
+                            c = par;
+                        }
+                        heap[c] = key;
+                    } else if (key < heap[0]) {  // replace top + sift down (128-131)
+                        int c = 0;
+                        while (true) {
+                            const int l = 2 * c + 1, r = l + 1;
+                            if (l >= k) break;
+                            int m = l;
+                            uint64_t mk = heap[l];
+                            if (r < k) {
+                                const uint64_t rk = heap[r];
+                                if (rk > mk) {
+                                    m = r;
+                                    mk = rk;
+                                }
+                            }
+                            if (mk <= key) break;
+                            heap[c] = mk;
+                            c = m;
+                        }
+                        heap[c] = key;
+                    }
+                    if (count == k) r2 = key_dist(heap[0]);
+                }
+            }
+            cnt.step(1, 1, from_parent ? 1 : 0);
+            const float sd = __fsub_rn(__ldg(qp + d), __ldg(node + d));
+            const int cs = sd > 0.0f;
+            const bool fir = __fmul_rn(sd, sd) <= r2;
+            const int32_t parent = ((curr + 1) >> 1) - 1;
+            int32_t next;
+            if constexpr (!UNORDERED) {
+                const int32_t close = 2 * curr + 1 + cs;
+                const int32_t far = 2 * curr + 2 - cs;
+                next = from_parent ? close : ((prev == close && fir) ? far : parent);
+                if (next >= n) {
+                    cnt.step(2, 1, 0);
+                    next = (next == close && fir) ? far : parent;
+                    if (next >= n) {
+                        cnt.step(2, 1, 0);
+                        next = parent;
+                    }
+                }
+            } else {
+                const int32_t left = 2 * curr + 1, right = 2 * curr + 2;
+                const bool enter_left = !cs || fir, enter_right = cs || fir;
+                if (from_parent)
+                    next = enter_left ? left : (enter_right ? right : parent);
+                else
+                    next = (prev == left && enter_right) ? right : parent;
+                if (next >= n) {
+                    cnt.step(2, 1, 0);
+                    next = (next == left && enter_right) ? right : parent;
+                    if (next >= n) {
+                        cnt.step(2, 1, 0);
+                        next = parent;
+                    }
+                }
+            }
+            if (next < 0) break;
+            prev = curr;
+            curr = next;
+        }
+        // heap sort ascending in place (extract_sorted, traverse.cpp:18-23)
+        for (int end = count - 1; end > 0; --end) {
+            const uint64_t top = heap[0];
+            const uint64_t x = heap[end];
+            heap[end] = top;
+            int c = 0;
+            while (true) {
+                const int l = 2 * c + 1, r = l + 1;
+                if (l >= end) break;
+                int m = l;
+                uint64_t mk = heap[l];
+                if (r < end) {
+                    const uint64_t rk = heap[r];
+                    if (rk > mk) {
+                        m = r;
+                        mk = rk;
+                    }
+                }
+                if (mk <= x) break;
+                heap[c] = mk;
+                c = m;
+            }
+            heap[c] = x;
+        }
+        int2* out = reinterpret_cast<int2*>(heap);
+        for (int j = 0; j < k; ++j) {
+            const uint64_t key = j < count ? heap[j] : kEmptyKey;
+            out[j] = make_int2(int32_t(uint32_t(key)), int32_t(uint32_t(key >> 32) - 1u));
+        }
+        a.counts[qi] = count;
+    }
+    flush_stats<STATS>(a, qi, active, cnt);
+}
+
+// Host-side dispatch (walk_dispatch.cu).  Returns the number of launches.
+int launch_walk(const WalkArgs& a, int dim, int layout_stride, bool stats, bool unordered,
+                cudaStream_t stream);
+
+// Register-list capacity used for k (0 = heap kernel).
+int walk_bucket(int k);
+
+}  // namespace fkd

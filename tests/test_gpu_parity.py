@@ -1,0 +1,196 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Bit-exact bar: counts exact, hit nodes and dist2 bits
+identical, per-query nodes_processed/visited/steps identical to the
+reference's stack-free walk (traverse.hpp:198-248), result_hash equal.
+"""
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+import paper_2210_12859_b200 as fk
+
+pytestmark = pytest.mark.gpu
+
+INF = float("inf")
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _kind(k):
+    return fk.QueryKind.knn if k > 0 else fk.QueryKind.fcp
+
+
+def _run_both(oracle, nodes, qs, k, r, morton=True, engine=0):
+    """k == 0 -> fcp.  Returns (gpu BatchResult, oracle tuple)."""
+    tree = fk.KdTree.from_level_order(nodes)
+    opt = fk.BatchOptions(kind=_kind(k), k=max(k, 1), max_radius=r, collect_stats=True,
+                          morton=morton, engine=fk.Engine(engine))
+    res = fk.run_batch(tree, qs, opt)
+    ref = oracle.run_batch(nodes, qs, "knn" if k > 0 else "fcp", max(k, 1), r,
+                           recursive=bool(engine), per_query=True)
+    return res, ref
+
+
+def _assert_same(res, ref, what=""):
+    c, h, st, _ = ref
+    assert np.array_equal(res.counts, c), f"counts differ {what}"
+    if res.hits.tobytes() != h.tobytes():
+        bad = np.nonzero(res.hits.view(np.uint64) != h.view(np.uint64))[0][:5]
+        raise AssertionError(f"hits differ {what} at {bad}: gpu={res.hits[bad]} ref={h[bad]}")
+    assert (res.stats.steps, res.stats.nodes_visited, res.stats.nodes_processed) == \
+        (int(st["steps"]), int(st["nodes_visited"]), int(st["nodes_processed"])), f"stats {what}"
+
+
+def test_figure1_goldens():
+    # SPEC.md:141-171, selfcheck.cpp:268-274 (Fig. 1 of the paper)
+    pts = np.array([[2, 3], [5, 4], [9, 6], [4, 7], [8, 1], [7, 2]], np.float32)
+    nodes = fk.build_level_order(pts)
+    assert nodes.tolist() == [[7, 2], [5, 4], [9, 6], [2, 3], [4, 7], [8, 1]]
+    tree = fk.KdTree.from_level_order(nodes)
+    hit, st = fk.fcp(tree, [9, 2], stats=True)
+    assert hit == (5, 2.0)
+    assert (st.steps, st.nodes_visited, st.nodes_processed) == (9, 7, 3)
+    assert fk.fcp(tree, [2, 3]) == (3, 0.0)
+    assert fk.knn(tree, [9, 2], 2) == [(5, 2.0), (0, 4.0)]
+    assert fk.fcp(tree, [9, 2], max_radius=1.0) is None
+    res = fk.run_batch(tree, np.array([[9, 2], [2, 3]], np.float32),
+                       fk.BatchOptions(kind=fk.QueryKind.knn, k=3))
+    assert fk.write_query_results(res) == "3,5,1.41421354,0,2,2,4\n3,3,0,1,3.1622777,4,4.47213602\n"
+
+
+@pytest.mark.parametrize("dim", [1, 2, 3, 4, 5, 8, 9])
+def test_uniform_all_configs(oracle, dim):
+    n, m = 5000, 3000
+    nodes = oracle.build_tree(oracle.random_points(100 + dim, n, dim))
+    qs = oracle.random_points(200 + dim, m, dim) * np.float32(1.2) - np.float32(0.1)
+    for k in (0, 1, 2, 3, 4, 8, 16, 20, 33, 50, 64, 65, 100):
+        for r in (INF, 0.25, 0.01, 0.0):
+            res, ref = _run_both(oracle, nodes, qs, k, r)
+            _assert_same(res, ref, f"dim={dim} k={k} r={r}")
+
+
+def test_tie_heavy_instances(oracle):
+    """instancegen-style trees (grid snap, duplicates) and queries (exact hits,
+    on-plane) — the cases that pin hit_order (SURVEY §8(c) tie coverage)."""
+    rng = oracle.instance_rng(4242)
+    for t in range(120):
+        n = rng.next_int(0, 2500)
+        dim = rng.next_int(1, 6)
+        grid = (8 if rng.chance(0.5) else 16) if rng.chance(0.6) else 0
+        dup = 0.2 if rng.chance(0.5) else 0.0
+        pts = rng.random_point_set(n, dim, grid, dup)
+        nodes = oracle.build_tree(pts) if n else pts
+        qs = np.stack([rng.random_query(dim, pts) for _ in range(200)])
+        for k in (0, 1, 4, 8, 20, 50):
+            r = (INF, 0.25, 0.01, 0.0)[rng.next_int(0, 3)]
+            res, ref = _run_both(oracle, nodes.reshape(n, dim), qs, k, r, morton=bool(t % 2))
+            _assert_same(res, ref, f"tree#{t} n={n} dim={dim} k={k} r={r}")
+
+
+def test_recursive_engine_stats(oracle):
+    nodes = oracle.build_tree(oracle.random_points(5, 3000, 3))
+    qs = oracle.random_points(6, 2000, 3)
+    for k in (0, 8):
+        res, ref = _run_both(oracle, nodes, qs, k, 0.1, engine=1)
+        _assert_same(res, ref, f"recursive k={k}")
+
+
+def test_per_query_stats_device(oracle):
+    import torch
+
+    nodes = oracle.build_tree(oracle.random_points(9, 20000, 3))
+    qs = oracle.random_points(10, 5000, 3)
+    tree = fk.KdTree.from_level_order(nodes)
+    dq = torch.from_numpy(qs).cuda()
+    counts = torch.empty(5000, dtype=torch.int32, device="cuda")
+    hits = torch.empty(5000 * 8, dtype=torch.int64, device="cuda")
+    pq = torch.empty(5000 * 3, dtype=torch.int64, device="cuda")
+    st, tm = fk.run_batch_device(tree, dq, counts, hits, fk.BatchOptions(kind=fk.QueryKind.knn, k=8,
+                                 collect_stats=True), per_query=pq, timings=True)
+    c, h, tot, per = oracle.run_batch(nodes, qs, "knn", 8, INF, per_query=True)
+    assert np.array_equal(counts.cpu().numpy(), c)
+    assert hits.cpu().numpy().tobytes() == h.tobytes()
+    got = pq.cpu().numpy().reshape(-1, 3)
+    assert np.array_equal(got[:, 2], per["nodes_processed"])
+    assert np.array_equal(got[:, 1], per["nodes_visited"])
+    assert np.array_equal(got[:, 0], per["steps"])
+    assert tm["walk_launches"] >= 1
+
+
+def test_unordered_matches_brute_force(oracle):
+    for dim in (2, 4, 8):
+        nodes = oracle.build_tree(oracle.random_points(30 + dim, 4000, dim))
+        qs = oracle.random_points(40 + dim, 1000, dim)
+        tree = fk.KdTree.from_level_order(nodes)
+        for k, r in ((16, INF), (16, 0.2), (1, INF)):
+            opt = fk.BatchOptions(kind=fk.QueryKind.knn, k=k, max_radius=r, unordered=True)
+            res = fk.run_batch(tree, qs, opt)
+            c, h = oracle.brute_batch(nodes, qs, "knn", k, r)
+            assert np.array_equal(res.counts, c)
+            assert res.hits.tobytes() == h.tobytes()
+
+
+@pytest.mark.parametrize("k,r,golden", [
+    (0, INF, 0x79446ad66bb295e9),   # C1 fcp 3D N=1M M=1M
+    (8, INF, 0x220c5639002591a1),   # kNN8 maxR=inf
+    (8, 0.01, 0xd50e9239b721b47a),  # kNN8 maxR=0.01
+])
+def test_c1_c2_golden_hashes(k, r, golden):
+    data = fk.random_points(1, 1, 1_000_000, 3)
+    qs = fk.random_points(1, 2, 1_000_000, 3)
+    tree = fk.build_tree(data)
+    res = fk.run_batch(tree, qs, fk.BatchOptions(kind=_kind(k), k=max(k, 1), max_radius=r,
+                                                 collect_stats=True))
+    assert res.result_hash() == golden
+    if k == 0:
+        assert (res.stats.steps, res.stats.nodes_visited, res.stats.nodes_processed) == \
+            (108117642, 96233846, 42675025)
+
+
+def test_edge_cases(oracle):
+    tree = fk.KdTree.from_level_order(np.zeros((0, 3), np.float32))
+    res = fk.run_batch(tree, np.full((4, 3), np.nan, np.float32), fk.BatchOptions(kind=fk.QueryKind.knn, k=3))
+    assert res.counts.tolist() == [0] * 4 and (res.hits["node"] == -1).all() and np.isinf(res.hits["dist2"]).all()
+    nodes = oracle.build_tree(oracle.random_points(3, 100, 3))
+    tree = fk.KdTree.from_level_order(nodes)
+    assert fk.run_batch(tree, np.zeros((0, 3), np.float32)).counts.size == 0
+    qs = oracle.random_points(4, 10, 3)
+    qs[7, 1] = np.inf
+    qs[9, 0] = np.nan
+    with pytest.raises(fk.DataError, match="queries: non-finite coordinate in point 7"):
+        fk.run_batch(tree, qs)
+    with pytest.raises(fk.DataError, match="query dimension 2 does not match tree dimension 3"):
+        fk.run_batch(tree, np.zeros((5, 2), np.float32))
+    with pytest.raises(fk.InvalidArgument):
+        fk.run_batch(tree, qs, fk.BatchOptions(kind=fk.QueryKind.knn, k=0))
+    with pytest.raises(fk.DataError, match="max radius"):
+        fk.run_batch(tree, qs, fk.BatchOptions(max_radius=float("nan")))
+    with pytest.raises(fk.DataError, match="tree nodes: non-finite coordinate in point 1"):
+        fk.KdTree.from_level_order(np.array([[0, 0], [np.inf, 1]], np.float32))
+    # single-query validation order: radius before k (traverse.hpp:115-117)
+    with pytest.raises(fk.DataError):
+        fk.knn(tree, [0, 0, 0], 0, max_radius=-1.0)
+
+
+def test_device_tree_and_path_match_host(oracle):
+    import torch
+
+    pts = oracle.random_points(77, 30000, 3)
+    nodes = oracle.build_tree(pts)
+    t_host = fk.KdTree.from_level_order(nodes)
+    t_dev = fk.KdTree.from_device(torch.from_numpy(nodes).cuda())
+    qs = oracle.random_points(78, 10000, 3)
+    a = fk.run_batch(t_host, qs, fk.BatchOptions(kind=fk.QueryKind.knn, k=4, max_radius=0.05))
+    b = fk.run_batch(t_dev, qs, fk.BatchOptions(kind=fk.QueryKind.knn, k=4, max_radius=0.05))
+    assert a.hits.tobytes() == b.hits.tobytes() and np.array_equal(a.counts, b.counts)
+
+
+def test_cpp_shim_against_reference():
+    exe = os.path.join(ROOT, "tests", "cpp", "shim_parity")
+    if not os.path.exists(exe):
+        pytest.skip("shim_parity not built (needs the reference headers at build time)")
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "OK" in out.stdout
