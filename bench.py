@@ -1,0 +1,408 @@
+#!/usr/bin/env python3
+"""Benchmark: fcp + kNN(k=8) queries/s on B200 (BASELINE.json metric).
+
+Workload (default ``c3``, BASELINE.json configs[2]): 3-D float, N = 10M
+points from 64 Gaussian blobs (sigma 0.02), M = 10M queries from the same
+mixture, walked in Morton order.  One *step* = one fcp batch over the M
+queries + one unbounded kNN(k=8) batch over the same M queries, each a full
+``fkd_run_batch_device`` call (Morton keys + radix sort + walk).  ``value``
+= 2*M*N_gpus / step time with inputs resident in HBM; ``e2e`` = the same
+through the host-buffer C ABI call ``fkd_run_batch`` (H2D + walk + D2H
+inside the timed region, pinned host buffers).
+
+Multi-GPU (torchrun): one rank per GPU, the tree is built on rank 0 and
+replicated with an NCCL broadcast; every rank walks its own M queries
+(weak scaling, no per-query communication); time = max over ranks.
+
+``--impl reference`` times the reference's own ``flatkd::run_batch``
+(oracle/_ref, compiled unmodified from the reference sources) with all
+host threads on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: (description, N, M, dim, generator, [(kind, k, max_radius), ...])
+    "c3": ("fcp + kNN8 3D, N=10M clustered (64 Gaussian blobs, sigma=0.02), M=10M queries "
+           "from the same mixture, Morton-ordered", 10_000_000, 10_000_000, 3, "clustered",
+           [("fcp", 1, float("inf")), ("knn", 8, float("inf"))]),
+    "c3u": ("fcp + kNN8 3D, N=10M uniform, M=10M uniform queries, Morton-ordered",
+            10_000_000, 10_000_000, 3, "uniform", [("fcp", 1, float("inf")), ("knn", 8, float("inf"))]),
+    "c1": ("fcp 3D, N=1M uniform, M=1M uniform queries", 1_000_000, 1_000_000, 3, "uniform",
+           [("fcp", 1, float("inf"))]),
+    "c2": ("kNN8 3D, N=1M uniform, M=1M queries, maxR=0.01", 1_000_000, 1_000_000, 3, "uniform",
+           [("knn", 8, 0.01)]),
+}
+SEED = 1
+METRIC = "fcp & kNN(k=8) queries/sec, 3D float, N=10M, 1/2/4/8 B200 vs host CPU"
+
+
+def gen_points(fk, kind: str, stream: int, count: int, dim: int) -> np.ndarray:
+    if kind == "clustered":
+        return fk.clustered_points(SEED, stream, count, dim, 64, 0.02)
+    return fk.random_points(SEED, stream, count, dim)
+
+
+def bytes_per_query(dim: int, p_bar: float, stride: int) -> float:
+    """Algorithmic bytes: query + every processed point once
+    + count + hit slots."""
+    return 4 * dim + p_bar * 4 * dim + 4 + 8 * stride
+
+
+def measured_peaks() -> tuple[float, str]:
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(workload: str):
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(workload)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = f"/tmp/fkd_clocks_{os.getpid()}.csv"
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.f.close()
+
+    def summary(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        rows = []
+        try:
+            for line in open(self.path):
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) == 6 and parts[0].isdigit():
+                    rows.append(parts)
+        except Exception:
+            pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": float(statistics.median(float(r[0]) for r in rows)),
+                "sm_max_mhz": float(max(float(r[1]) for r in rows)), "reasons": reasons,
+                "samples": len(rows)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ----------------------------------------------------------------------------- reference arm
+
+def run_reference(args) -> None:
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    import paper_2210_12859_b200 as fk  # generators only (input data, not the path)
+    from oracle import Reference
+    from paper_2210_12859_b200.shard import query_stream
+
+    desc, n, m, dim, gkind, batches = WORKLOADS[args.workload]
+    ref = Reference()
+    threads = ref.hardware_threads()
+    pts = gen_points(fk, gkind, 1, n, dim)
+    nodes = ref.build_tree(pts)  # flatkd::build_tree (untimed, as bench.cpp does)
+    sample = min(m, args.ref_sample)
+    qs = gen_points(fk, gkind, query_stream(0), m, dim)[:sample]
+    times = []
+    for it in range(args.warmup + args.steps):
+        t = 0.0
+        for kind, k, r in batches:
+            _, _, _, secs = ref.run_batch(nodes, qs, kind, k, r, threads=0)
+            t += secs
+        if it >= args.warmup:
+            times.append(t)
+    step = float(np.mean(times))
+    value = len(batches) * sample / step
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": step * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": desc, "sample_queries_per_batch": sample, "tree_n": n,
+                   "batches": [f"{k_}{'' if k_ == 'fcp' else kk}" for k_, kk, _ in batches]},
+        "cpu_baseline": {"value": value, "unit": "queries/s", "cores": threads, "kind": "reference",
+                         "sample": f"first {sample} of the {m} queries, each batch of the step, "
+                                   "flatkd::run_batch (Engine::stack_free, OpenMP all threads)"},
+        "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- B200 arm
+
+def cpu_baseline_leg(fk, nodes, qs_host, batches, sample, gpu_tree) -> dict:
+    """The reference run_batch on the host cores, same tree/queries (sample),
+    plus a parity check of the GPU results on that sample."""
+    from oracle import REF_SO, Oracle, Reference
+
+    kind_name = "reference" if os.path.exists(REF_SO) else "port"
+    impl = Reference() if kind_name == "reference" else Oracle()
+    q = np.ascontiguousarray(qs_host[:sample])
+    total_t = 0.0
+    parity = True
+    for kind, k, r in batches:
+        if kind_name == "reference":
+            c, h, _, secs = impl.run_batch(nodes, q, kind, k, r, threads=0)
+            ref_hash = impl.result_hash(c, h, k if kind == "knn" else 1)
+        else:
+            t0 = time.perf_counter()
+            c, h, _, _ = impl.run_batch(nodes, q, kind, k, r, threads=0)
+            secs = time.perf_counter() - t0
+            ref_hash = impl.result_hash(c, h, k if kind == "knn" else 1)
+        total_t += secs
+        res = fk.run_batch(gpu_tree, q, fk.BatchOptions(kind=fk.QueryKind[kind], k=k, max_radius=r))
+        parity &= res.result_hash() == ref_hash
+    cores = os.cpu_count() or 1
+    return {"value": len(batches) * sample / total_t, "unit": "queries/s", "cores": cores,
+            "kind": kind_name, "parity_hash_equal": bool(parity),
+            "sample": f"first {sample} queries of rank 0, every batch of the step, "
+                      f"{'flatkd::run_batch from oracle/_ref' if kind_name == 'reference' else 'oracle port'}"
+                      f" with {cores} OpenMP threads"}
+
+
+def run_b200(args) -> None:
+    import torch
+
+    import paper_2210_12859_b200 as fk
+    from paper_2210_12859_b200.shard import max_over_ranks, query_stream, replicate_tree
+
+    world, rank, local = dist_env()
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    desc, n, m, dim, gkind, batches = WORKLOADS[args.workload]
+
+    # ---- tree: built on rank 0, replicated by NCCL broadcast
+    nodes_host = fk.build_level_order(gen_points(fk, gkind, 1, n, dim)) if rank == 0 else None
+    nodes_dev = replicate_tree(nodes_host, n, dim, dev)
+    tree = fk.KdTree.from_device(nodes_dev)
+
+    qs_host = gen_points(fk, gkind, query_stream(rank), m, dim)
+    qs_dev = torch.from_numpy(qs_host).to(dev)
+    outs = {}
+    for kind, k, _ in batches:
+        outs[(kind, k)] = (torch.empty(m, dtype=torch.int32, device=dev),
+                           torch.empty(m * k, dtype=torch.int64, device=dev))
+    opts = [fk.BatchOptions(kind=fk.QueryKind[kind], k=k, max_radius=r) for kind, k, r in batches]
+
+    # ---- untimed stats pass: P-bar per batch (algorithmic bytes)
+    pbar = {}
+    for (kind, k, r), o in zip(batches, opts):
+        c, h = outs[(kind, k)]
+        st, _ = fk.run_batch_device(tree, qs_dev, c, h, fk.BatchOptions(kind=o.kind, k=k, max_radius=r,
+                                                                        collect_stats=True))
+        pbar[(kind, k)] = st.nodes_processed / m
+
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # 256 MB > L2
+    stream = torch.cuda.current_stream()
+
+    def step(timing: bool):
+        tms = []
+        for (kind, k, _), o in zip(batches, opts):
+            c, h = outs[(kind, k)]
+            _, tm = fk.run_batch_device(tree, qs_dev, c, h, o, stream=stream, timings=timing)
+            tms.append(tm)
+        return tms
+
+    for _ in range(args.warmup):
+        step(False)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    step_ms, walk_ms, launches = [], {b: [] for b in range(len(batches))}, 0
+    sampler = ClockSampler(dev.index)
+    with sampler:
+        for _ in range(args.steps):
+            flush.zero_()  # untimed L2 flush between timed steps
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            tms = step(True)
+            e1.record(stream)
+            e1.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+            for b, tm in enumerate(tms):
+                walk_ms[b].append(tm["walk_ms"])
+                launches += tm["launches"]
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    t_step = max_over_ranks(sum(step_ms), dev) / args.steps / 1e3  # seconds, max over ranks
+    value = world * len(batches) * m / t_step
+
+    # ---- e2e through the host-buffer C ABI (pinned buffers), same metric
+    import ctypes as C
+
+    hq = fk.LIB.fkd_host_alloc(qs_host.nbytes)
+    C.memmove(hq, qs_host.ctypes.data, qs_host.nbytes)
+    host_out = {}
+    for kind, k, _ in batches:
+        host_out[(kind, k)] = (fk.LIB.fkd_host_alloc(m * 4), fk.LIB.fkd_host_alloc(m * k * 8))
+    h2d = d2h = 0
+    for kind, k, _ in batches:
+        h2d += m * dim * 4
+        d2h += m * 4 + m * k * 8
+
+    def e2e_step():
+        for (kind, k, _), o in zip(batches, opts):
+            hc, hh = host_out[(kind, k)]
+            co = o.to_c()
+            rc = fk.LIB.fkd_run_batch(tree.handle, hq, m, dim, C.byref(co), hc, hh, None)
+            if rc != 0:
+                raise RuntimeError(fk.LIB.fkd_last_error().decode())
+
+    for _ in range(max(1, args.warmup)):
+        e2e_step()
+    if dist is not None:
+        dist.barrier()
+    e2e_times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        e2e_step()
+        e2e_times.append(time.perf_counter() - t0)
+    e2e_value = world * len(batches) * m / (max_over_ranks(sum(e2e_times), dev) / args.steps)
+    # results of the e2e path must equal the device path (same queries)
+    e2e_parity = True
+    for kind, k, _ in batches:
+        hc, hh = host_out[(kind, k)]
+        c, h = outs[(kind, k)]
+        got_c = np.ctypeslib.as_array(C.cast(hc, C.POINTER(C.c_int32)), shape=(m,))
+        e2e_parity &= bool(np.array_equal(got_c, c.cpu().numpy()))
+    for hc, hh in host_out.values():
+        fk.LIB.fkd_host_free(hc)
+        fk.LIB.fkd_host_free(hh)
+    fk.LIB.fkd_host_free(hq)
+
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel (largest walk time)
+    peak, peak_src = measured_peaks()
+    dom = max(range(len(batches)), key=lambda b: float(np.mean(walk_ms[b])))
+    kind, k, r = batches[dom]
+    stride = k if kind == "knn" else 1
+    bq = bytes_per_query(dim, pbar[(kind, k)], stride)
+    t_walk = float(np.mean(walk_ms[dom])) / 1e3
+    achieved = m * bq / t_walk / 1e9
+    traffic = ncu_traffic(args.workload)
+    per_batch = {}
+    for b, (kk, k2, r2) in enumerate(batches):
+        name = kk if kk == "fcp" else f"knn{k2}"
+        tw = float(np.mean(walk_ms[b])) / 1e3
+        per_batch[name] = {"walk_ms": tw * 1e3, "walk_qps": m / tw, "P_bar": pbar[(kk, k2)],
+                           "bytes_per_query": bytes_per_query(dim, pbar[(kk, k2)], k2 if kk == "knn" else 1),
+                           "hbm_frac": m * bytes_per_query(dim, pbar[(kk, k2)], k2 if kk == "knn" else 1) / tw / 1e9 / peak}
+
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_leg(fk, nodes_host, qs_host, batches, min(m, args.cpu_sample), tree)
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": desc, "tree_n": n, "queries_per_gpu": m, "dim": dim,
+                   "batches_per_step": [("fcp" if kk == "fcp" else f"knn{k2}") for kk, k2, _ in batches],
+                   "max_radius": [rr for _, _, rr in batches], "parallelism": f"query-sharded x{world}",
+                   "l2": "256 MB buffer written between timed steps (untimed); inputs 120+160 MB > L2",
+                   "morton": True},
+        "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "results_equal_device_path": bool(e2e_parity),
+                "path": "fkd_run_batch (C ABI, pinned host buffers, chunked H2D/walk/D2H)"},
+        "gpu_launches": launches // args.steps,
+        "gpu_launches_note": "own kernels per timed step (Morton keys + walk per batch); CUB sort kernels excluded",
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": f"walk {kind}{'' if kind == 'fcp' else k} (dominant)",
+                     "peak_source": peak_src,
+                     "algorithmic_bytes_per_query": bq},
+        "per_batch": per_batch,
+        "clocks": sampler.summary(),
+    }
+    if cpu is not None:
+        line["cpu_baseline"] = cpu
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c3")
+    ap.add_argument("--cpu-sample", type=int, default=1_000_000)
+    ap.add_argument("--ref-sample", type=int, default=1_000_000)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

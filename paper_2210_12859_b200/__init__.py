@@ -196,7 +196,10 @@ class KdTree:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h:
-            LIB.fkd_tree_destroy(h)
+            try:
+                LIB.fkd_tree_destroy(h)
+            except Exception:  # interpreter shutdown
+                pass
             self._h = None
 
     def size(self) -> int:
@@ -234,12 +237,12 @@ def build_level_order(points) -> np.ndarray:
 def run_batch(tree: KdTree, queries, options: Optional[BatchOptions] = None) -> BatchResult:
     """flatkd::run_batch (batch.cpp:71-134) on the GPU, host buffers in and out."""
     options = options or BatchOptions()
+    if options.kind == QueryKind.knn and options.k < 1:  # batch.cpp:72-73, checked first
+        raise InvalidArgument("knn: k must be >= 1")
     q = _f32(queries, tree.dim())
     if q.ndim != 2:
         raise DataError("queries: expected an (m, dim) array")
     m, dim = q.shape
-    if options.kind == QueryKind.knn and options.k < 1:
-        raise InvalidArgument("knn: k must be >= 1")
     stride = options.stride
     counts = np.zeros(m, np.int32)
     hits = np.empty(m * stride, HIT_DTYPE)

@@ -38,6 +38,25 @@ fkd_status fail(fkd_status s, const std::string& msg) {
 
 constexpr int64_t kSortChunk = int64_t(1) << 30;  // u32 ids, int item counts in CUB
 
+struct Tuning {
+    int persistent = 0;
+    int chunk = 64;
+    int refill = 8;
+};
+
+// Launch tuning, overridable for experiments: FKD_PERSIST=0|1,
+// FKD_WORK_CHUNK=<positions per fetch>, FKD_REFILL=<idle lanes>.
+const Tuning& tuning() {
+    static const Tuning t = [] {
+        Tuning x;
+        if (const char* e = std::getenv("FKD_PERSIST")) x.persistent = std::atoi(e) != 0;
+        if (const char* e = std::getenv("FKD_WORK_CHUNK")) x.chunk = std::max(32, std::atoi(e));
+        if (const char* e = std::getenv("FKD_REFILL")) x.refill = std::min(32, std::max(1, std::atoi(e)));
+        return x;
+    }();
+    return t;
+}
+
 // Store layout: padded vectors (1, 2, 4, 4, 8, 8, 8, 8 floats) by default;
 // FKD_LAYOUT=packed keeps 3-D nodes at 12 bytes (chosen
 // by measurement).
@@ -65,7 +84,7 @@ struct Workspace {
     int64_t key_cap = 0;
     void* sort_tmp = nullptr;
     size_t sort_tmp_bytes = 0;
-    unsigned long long* small = nullptr;    // [4]: bad, steps, visited, processed
+    unsigned long long* small = nullptr;    // [8]: bad, steps, visited, processed, work counter
     unsigned long long* h_small = nullptr;  // pinned mirror
     // host-path staging
     float* q = nullptr;
@@ -162,8 +181,8 @@ fkd_status acquire_ws(Replica& r, Workspace** out) {
     cudaError_t e = cudaStreamCreateWithFlags(&w->stream, cudaStreamNonBlocking);
     for (auto& ev : w->ev)
         if (e == cudaSuccess) e = cudaEventCreate(&ev);
-    if (e == cudaSuccess) e = cudaMalloc(&w->small, 4 * sizeof(unsigned long long));
-    if (e == cudaSuccess) e = cudaMallocHost(&w->h_small, 4 * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMalloc(&w->small, 8 * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMallocHost(&w->h_small, 8 * sizeof(unsigned long long));
     if (e != cudaSuccess) {
         delete w;
         return fail(FKD_CUDA_ERROR, std::string("workspace: ") + cudaGetErrorString(e));
@@ -266,6 +285,10 @@ fkd_status enqueue(const fkd_tree* t, Replica& r, Workspace* w, const float* d_q
         a.per_query = d_per_query ? d_per_query + base : nullptr;
         a.bad = w->small;
         a.id_base = base;
+        a.work = w->small + 4;
+        a.chunk = tuning().chunk;
+        a.refill = tuning().refill;
+        a.persistent = tuning().persistent;
         if (sort) {
             const int64_t half = w->key_cap / 2;
             const int rc = morton_order(a.queries, cm, t->dim, t->frame, w->keys, w->keys + half,
@@ -275,6 +298,7 @@ fkd_status enqueue(const fkd_tree* t, Replica& r, Workspace* w, const float* d_q
             a.order = w->ids + half;
         }
         if (ev_mid && base == 0) FKD_CUDA(cudaEventRecord(ev_mid, st));
+        if (a.persistent) FKD_CUDA(cudaMemsetAsync(a.work, 0, sizeof(unsigned long long), st));
         const int nl = launch_walk(a, t->dim, t->stride, stats, (o->flags & FKD_FLAG_UNORDERED) != 0, st);
         if (nl <= 0) return fail(FKD_CUDA_ERROR, "no kernel for this configuration");
         *launches += nl;
@@ -531,7 +555,7 @@ fkd_status fkd_run_batch_device(const fkd_tree* t, const float* d_q, int64_t m, 
     Workspace* w = nullptr;
     if ((s = acquire_ws(r, &w)) != FKD_OK) return s;
     const bool want_stats = stats != nullptr || d_per_query != nullptr;
-    const unsigned long long init[4] = {kNoBad, 0, 0, 0};
+    const unsigned long long init[8] = {kNoBad, 0, 0, 0, 0, 0, 0, 0};
     int launches = 0, walk_launches = 0;
     auto body = [&]() -> fkd_status {
         FKD_CUDA(cudaMemcpyAsync(w->small, init, sizeof(init), cudaMemcpyHostToDevice, st));
@@ -605,7 +629,7 @@ fkd_status fkd_run_batch(const fkd_tree* t, const float* queries, int64_t m, int
             jobs.push_back(Job{di, wss[di][c % wss[di].size()], b, std::min(kChunk, hi - b)});
         }
     }
-    std::vector<unsigned long long> small(jobs.size() * 4, 0);
+    std::vector<unsigned long long> small(jobs.size() * 8, 0);
     if (err == FKD_OK) {
         // size every workspace for its largest chunk before enqueueing
         for (int di = 0; di < ndev && err == FKD_OK; ++di) {
@@ -628,7 +652,7 @@ fkd_status fkd_run_batch(const fkd_tree* t, const float* queries, int64_t m, int
         Replica& r = *t->reps[j.rep];
         DeviceGuard g(r.device);
         Workspace* w = j.w;
-        const unsigned long long init[4] = {kNoBad, 0, 0, 0};
+        const unsigned long long init[8] = {kNoBad, 0, 0, 0, 0, 0, 0, 0};
         int launches = 0, wl = 0;
         auto step = [&]() -> fkd_status {
             FKD_CUDA(cudaMemcpyAsync(w->q, queries + j.base * dim, size_t(j.count) * dim * sizeof(float),
@@ -641,7 +665,7 @@ fkd_status fkd_run_batch(const fkd_tree* t, const float* queries, int64_t m, int
                                      cudaMemcpyDeviceToHost, w->stream));
             FKD_CUDA(cudaMemcpyAsync(hits + j.base * k, w->hits, size_t(j.count) * k * sizeof(fkd_hit),
                                      cudaMemcpyDeviceToHost, w->stream));
-            FKD_CUDA(cudaMemcpyAsync(&small[ji * 4], w->small, sizeof(init), cudaMemcpyDeviceToHost,
+            FKD_CUDA(cudaMemcpyAsync(&small[ji * 8], w->small, sizeof(init), cudaMemcpyDeviceToHost,
                                      w->stream));
             return FKD_OK;
         };
@@ -660,9 +684,9 @@ fkd_status fkd_run_batch(const fkd_tree* t, const float* queries, int64_t m, int
     if (err != FKD_OK) return err;
     unsigned long long bad = kNoBad, tot[3] = {0, 0, 0};
     for (size_t ji = 0; ji < jobs.size(); ++ji) {
-        const unsigned long long b = small[ji * 4];
+        const unsigned long long b = small[ji * 8];
         if (b != kNoBad) bad = std::min<unsigned long long>(bad, b + jobs[ji].base);
-        for (int c = 0; c < 3; ++c) tot[c] += small[ji * 4 + 1 + c];
+        for (int c = 0; c < 3; ++c) tot[c] += small[ji * 8 + 1 + c];
     }
     if (bad != kNoBad)
         return fail(FKD_DATA_ERROR, "queries: non-finite coordinate in point " + std::to_string(bad));

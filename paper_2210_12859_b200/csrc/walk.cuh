@@ -57,6 +57,10 @@ struct WalkArgs {
     fkd_query_stats* per_query; // [m] or null (STATS)
     unsigned long long* bad;    // min id of a non-finite query
     int64_t id_base;            // added to query ids reported through `bad`
+    unsigned long long* work;   // persistent kernel: next unclaimed walk position
+    int32_t chunk;              // persistent kernel: positions claimed per fetch
+    int32_t refill;             // persistent kernel: idle lanes that trigger a refill
+    int32_t persistent;         // launch the persistent lane-refill kernel
 };
 
 __device__ __forceinline__ uint64_t make_key(float d2, int32_t node) {
@@ -147,24 +151,168 @@ struct Counters {
     }
 };
 
-// Warp-aggregated totals + optional per-query record.
-template <bool STATS>
-__device__ __forceinline__ void flush_stats(const WalkArgs& a, int64_t qi, bool active,
-                                            const Counters<STATS>& c) {
-    if constexpr (STATS) {
-        unsigned long long s = c.steps, v = c.visited, p = c.processed;
-        if (a.recursive_stats) {
-            // Engine::recursive counts one step per call (traverse.hpp:265) and
-            // never revisits: steps = processed + bounces, visited = processed.
-            const unsigned long long bounces = s - v;
-            s = p + bounces;
-            v = p;
+// ---------------------------------------------------------------------------
+// Register-list walk, D in 1..8 compile-time, KB slots, k <= KB at run time.
+// One query's complete state; step() is one loop trip of the state machine.
+// ---------------------------------------------------------------------------
+template <int D>
+__device__ __forceinline__ int dim_up(int d) {  // split dim one level deeper
+    if constexpr (D == 1) return 0;
+    else if constexpr ((D & (D - 1)) == 0) return (d + 1) & (D - 1);
+    else return d == D - 1 ? 0 : d + 1;
+}
+
+template <int D>
+__device__ __forceinline__ int dim_down(int d) {  // split dim one level up
+    if constexpr (D == 1) return 0;
+    else if constexpr ((D & (D - 1)) == 0) return (d - 1) & (D - 1);
+    else return d == 0 ? D - 1 : d - 1;
+}
+
+template <int D, int S, int KB, bool STATS, bool UNORDERED>
+struct LaneWalk {
+    float q[D];
+    uint64_t L[KB];
+    int32_t curr, prev;
+    int d;  // split dim of curr, tracked incrementally (tree.hpp:27-29)
+    float r2;
+    int64_t qi;
+    Counters<STATS> cnt;
+
+    // Loads the query and resets the state (traverse.hpp:250-255).  Returns
+    // false (and flags the id) for a non-finite query (batch.cpp:79).
+    __device__ __forceinline__ bool init(const WalkArgs& a, int64_t pos) {
+        qi = a.order ? int64_t(__ldg(a.order + pos)) : pos;
+        const float* qp = a.queries + qi * D;
+        bool finite = true;
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            q[j] = __ldg(qp + j);
+            finite &= isfinite(q[j]);
         }
-        if (!active) s = v = p = 0;
-        if (active && a.per_query) {
-            a.per_query[qi].steps = (int64_t)s;
-            a.per_query[qi].nodes_visited = (int64_t)v;
-            a.per_query[qi].nodes_processed = (int64_t)p;
+        if (!finite) {
+            atomicMin(a.bad, (unsigned long long)(a.id_base + qi));
+            return false;
+        }
+        const int dummies = KB - a.k;
+#pragma unroll
+        for (int j = 0; j < KB; ++j) L[j] = j < dummies ? 0ull : kEmptyKey;
+        curr = 0;
+        prev = -1;
+        d = 0;
+        r2 = a.cap2;
+        cnt = Counters<STATS>();
+        return true;
+    }
+
+    // One transition of traverse_step (traverse.hpp:198-248) plus the
+    // in-register bounces.  Returns false once the root stepped to -1.
+    __device__ __forceinline__ bool step(const WalkArgs& a) {
+        const int32_t n = a.n;
+        const bool from_parent = prev < curr;
+        float p[D];
+        float pd;
+        if constexpr (S == D && D > 1) {
+            if (from_parent) {
+                load_point<D, S>(a.nodes, curr, p);
+                pd = pick(p, d);
+            } else {
+                pd = __ldg(a.nodes + size_t(curr) * S + d);
+            }
+        } else {
+            load_point<D, S>(a.nodes, curr, p);
+            pd = pick(p, d);
+        }
+        if (from_parent) {  // traverse.hpp:217-222
+            const float d2 = sq_dist(q, p);
+            const uint64_t key = make_key(d2, curr);
+            if (d2 <= a.cap2 && key < L[KB - 1]) {
+                list_insert(L, key);
+                r2 = fminf(a.cap2, key_dist(L[KB - 1]));
+            }
+        }
+        cnt.step(1, 1, from_parent ? 1 : 0);
+
+        const float sd = __fsub_rn(pick(q, d), pd);                // 226
+        const int cs = sd > 0.0f;                                  // 227
+        const bool fir = __fmul_rn(sd, sd) <= r2;                  // 230
+        const int32_t parent = ((curr + 1) >> 1) - 1;              // 205
+        int32_t next;
+        if constexpr (!UNORDERED) {
+            const int32_t close = 2 * curr + 1 + cs;               // 228
+            const int32_t far = 2 * curr + 2 - cs;                 // 229
+            next = from_parent ? close : ((prev == close && fir) ? far : parent);
+            if (next >= n) {  // empty slot: bounce + return visit, in registers
+                cnt.step(2, 1, 0);
+                next = (next == close && fir) ? far : parent;
+                if (next >= n) {
+                    cnt.step(2, 1, 0);
+                    next = parent;
+                }
+            }
+        } else {
+            // left-first order; a child is entered iff it is on the query's
+            // side or its plane is within the radius
+            const int32_t left = 2 * curr + 1, right = 2 * curr + 2;
+            const bool enter_left = !cs || fir, enter_right = cs || fir;
+            if (from_parent)
+                next = enter_left ? left : (enter_right ? right : parent);
+            else
+                next = (prev == left && enter_right) ? right : parent;
+            if (next >= n) {
+                cnt.step(2, 1, 0);
+                next = (next == left && enter_right) ? right : parent;
+                if (next >= n) {
+                    cnt.step(2, 1, 0);
+                    next = parent;
+                }
+            }
+        }
+        if (next < 0) return false;  // 240-244
+        d = next == parent ? dim_down<D>(d) : dim_up<D>(d);
+        prev = curr;
+        curr = next;
+        return true;
+    }
+
+    // fixed-stride slot in input order (batch.cpp:104-119)
+    __device__ __forceinline__ void finish(const WalkArgs& a) {
+        const int k = a.k;
+        const int dummies = KB - k;
+        int2* out = reinterpret_cast<int2*>(a.hits + qi * k);
+        int c = 0;
+#pragma unroll
+        for (int j = 0; j < KB; ++j) {
+            const int s = j - dummies;
+            if (s >= 0) {
+                const uint64_t key = L[j];
+                out[s] = make_int2(int32_t(uint32_t(key)), int32_t(uint32_t(key >> 32) - 1u));
+                c += uint32_t(key) != 0xFFFFFFFFu;
+            }
+        }
+        a.counts[qi] = c;
+        if constexpr (STATS) {
+            if (a.per_query) {
+                unsigned long long s = cnt.steps, v = cnt.visited;
+                if (a.recursive_stats) {
+                    s = cnt.processed + (s - v);
+                    v = cnt.processed;
+                }
+                a.per_query[qi].steps = (int64_t)s;
+                a.per_query[qi].nodes_visited = (int64_t)v;
+                a.per_query[qi].nodes_processed = (int64_t)cnt.processed;
+            }
+        }
+    }
+};
+
+template <bool STATS>
+__device__ __forceinline__ void add_totals(const WalkArgs& a, unsigned long long s,
+                                           unsigned long long v, unsigned long long p) {
+    if constexpr (STATS) {
+        if (a.recursive_stats) {  // traverse.hpp:262-283 counting
+            s = p + (s - v);
+            v = p;
         }
         for (int off = 16; off > 0; off >>= 1) {
             s += __shfl_down_sync(0xffffffffu, s, off);
@@ -179,126 +327,82 @@ __device__ __forceinline__ void flush_stats(const WalkArgs& a, int64_t qi, bool 
     }
 }
 
-// ---------------------------------------------------------------------------
-// Register-list walk, D in 1..8 compile-time, KB slots, k <= KB at run time.
-// ---------------------------------------------------------------------------
+// One thread per walk position (plain grid).
 template <int D, int S, int KB, bool STATS, bool UNORDERED>
 __global__ void __launch_bounds__(256) walk_kernel(const WalkArgs a) {
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    bool active = i < a.m;
-    int64_t qi = 0;
-    float q[D];
+    LaneWalk<D, S, KB, STATS, UNORDERED> w;
+    bool active = i < a.m && w.init(a, i);
     if (active) {
-        qi = a.order ? int64_t(a.order[i]) : i;
-        const float* qp = a.queries + qi * D;
-        bool finite = true;
-#pragma unroll
-        for (int j = 0; j < D; ++j) {
-            q[j] = __ldg(qp + j);
-            finite &= isfinite(q[j]);
+        if (a.n > 0)
+            while (w.step(a)) {
+            }
+        w.finish(a);
+    }
+    if (active) add_totals<STATS>(a, w.cnt.steps, w.cnt.visited, w.cnt.processed);
+    else add_totals<STATS>(a, 0, 0, 0);
+}
+
+// Persistent warps with lane refill.  Each warp takes chunks of walk
+// positions from a global counter; whenever at least `refill` lanes have
+// finished their query, those lanes start the next positions of the chunk
+// (order is preserved within a warp's chunk, so Morton neighbours stay
+// together).  Removes both the warp-level trip-count imbalance (a warp no
+// longer waits for its slowest query) and the grid tail.
+template <int D, int S, int KB, bool STATS, bool UNORDERED>
+__global__ void __launch_bounds__(256) walk_persistent_kernel(const WalkArgs a) {
+    unsigned long long* __restrict__ work = a.work;
+    const int chunk = a.chunk, refill = a.refill;
+    const unsigned lane = threadIdx.x & 31u;
+    const unsigned lt = (1u << lane) - 1u;
+    LaneWalk<D, S, KB, STATS, UNORDERED> w;
+    bool active = false;
+    int64_t cursor = 0, end = 0;  // warp-uniform
+    bool exhausted = false;
+    unsigned long long ts = 0, tv = 0, tp = 0;
+    while (true) {
+        const unsigned idle = __ballot_sync(0xffffffffu, !active);
+        if (!exhausted && (idle == 0xffffffffu || __popc(idle) >= refill)) {
+            const int need = __popc(idle);
+            const int r = __popc(idle & lt);
+            const int64_t avail = end - cursor;
+            int64_t mine = (!active && r < avail) ? cursor + r : -1;
+            if (need > avail) {
+                unsigned long long base = 0;
+                if (lane == 0) base = atomicAdd(work, (unsigned long long)chunk);
+                base = __shfl_sync(0xffffffffu, base, 0);
+                if (int64_t(base) >= a.m) {
+                    exhausted = true;
+                    cursor = end;
+                } else {
+                    const int64_t nb = int64_t(base);
+                    const int64_t ne = nb + chunk < a.m ? nb + chunk : a.m;
+                    if (!active && r >= avail && nb + (r - avail) < ne) mine = nb + (r - avail);
+                    cursor = nb + (need - avail);
+                    end = ne;
+                    if (cursor > end) cursor = end;
+                }
+            } else {
+                cursor += need;
+            }
+            if (mine >= 0) active = w.init(a, mine);
+            if (active && a.n == 0) {
+                w.finish(a);
+                active = false;
+            }
         }
-        if (!finite) {  // batch.cpp:79 -> DataError, reported by the host
-            atomicMin(a.bad, (unsigned long long)(a.id_base + qi));
+        if (exhausted && __all_sync(0xffffffffu, !active)) break;
+        if (active && !w.step(a)) {
+            w.finish(a);
+            if constexpr (STATS) {
+                ts += w.cnt.steps;
+                tv += w.cnt.visited;
+                tp += w.cnt.processed;
+            }
             active = false;
         }
     }
-    Counters<STATS> cnt;
-    if (active) {
-        uint64_t L[KB];
-        const int dummies = KB - a.k;
-#pragma unroll
-        for (int j = 0; j < KB; ++j) L[j] = j < dummies ? 0ull : kEmptyKey;
-        const float cap2 = a.cap2;
-        const int32_t n = a.n;
-        float r2 = cap2;
-
-        int32_t curr = 0, prev = -1;
-        while (n > 0) {
-            const bool from_parent = prev < curr;
-            const int d = split_dim<D>(curr);
-            float p[D];
-            float pd;
-            if constexpr (S == D && D > 1) {
-                // packed store: the full point only on first visits
-                if (from_parent) {
-                    load_point<D, S>(a.nodes, curr, p);
-                    pd = pick(p, d);
-                } else {
-                    pd = __ldg(a.nodes + size_t(curr) * S + d);
-                }
-            } else {
-                load_point<D, S>(a.nodes, curr, p);
-                pd = pick(p, d);
-            }
-            if (from_parent) {  // traverse.hpp:217-222
-                const float d2 = sq_dist(q, p);
-                const uint64_t key = make_key(d2, curr);
-                if (d2 <= cap2 && key < L[KB - 1]) {
-                    list_insert(L, key);
-                    r2 = fminf(cap2, key_dist(L[KB - 1]));
-                }
-            }
-            cnt.step(1, 1, from_parent ? 1 : 0);
-
-            const float sd = __fsub_rn(pick(q, d), pd);                // 226
-            const int cs = sd > 0.0f;                                  // 227
-            const bool fir = __fmul_rn(sd, sd) <= r2;                  // 230
-            const int32_t parent = ((curr + 1) >> 1) - 1;              // 205
-            int32_t next;
-            if constexpr (!UNORDERED) {
-                const int32_t close = 2 * curr + 1 + cs;               // 228
-                const int32_t far = 2 * curr + 2 - cs;                 // 229
-                if (from_parent)
-                    next = close;
-                else
-                    next = (prev == close && fir) ? far : parent;
-                if (next >= n) {  // empty slot: bounce + return visit, in registers
-                    cnt.step(2, 1, 0);
-                    next = (next == close && fir) ? far : parent;
-                    if (next >= n) {
-                        cnt.step(2, 1, 0);
-                        next = parent;
-                    }
-                }
-            } else {
-                // left-first order; a child is entered iff it is on the
-                // query's side or its plane is within the radius
-                const int32_t left = 2 * curr + 1, right = 2 * curr + 2;
-                const bool enter_left = !cs || fir, enter_right = cs || fir;
-                if (from_parent)
-                    next = enter_left ? left : (enter_right ? right : parent);
-                else
-                    next = (prev == left && enter_right) ? right : parent;
-                if (next >= n) {
-                    cnt.step(2, 1, 0);
-                    next = (next == left && enter_right) ? right : parent;
-                    if (next >= n) {
-                        cnt.step(2, 1, 0);
-                        next = parent;
-                    }
-                }
-            }
-            if (next < 0) break;  // 240-244: the root stepped to -1
-            prev = curr;
-            curr = next;
-        }
-
-        // fixed-stride slot in input order (batch.cpp:104-119)
-        const int k = a.k;
-        int2* out = reinterpret_cast<int2*>(a.hits + qi * k);
-        int c = 0;
-#pragma unroll
-        for (int j = 0; j < KB; ++j) {
-            const int s = j - dummies;
-            if (s >= 0) {
-                const uint64_t key = L[j];
-                out[s] = make_int2(int32_t(uint32_t(key)), int32_t(uint32_t(key >> 32) - 1u));
-                c += uint32_t(key) != 0xFFFFFFFFu;
-            }
-        }
-        a.counts[qi] = c;
-    }
-    flush_stats<STATS>(a, qi, active, cnt);
+    add_totals<STATS>(a, ts, tv, tp);
 }
 
 // ---------------------------------------------------------------------------
@@ -452,8 +556,21 @@ __global__ void __launch_bounds__(128) walk_heap_kernel(const WalkArgs a) {
             out[j] = make_int2(int32_t(uint32_t(key)), int32_t(uint32_t(key >> 32) - 1u));
         }
         a.counts[qi] = count;
+        if constexpr (STATS) {
+            if (a.per_query) {
+                unsigned long long st = cnt.steps, v = cnt.visited;
+                if (a.recursive_stats) {
+                    st = cnt.processed + (st - v);
+                    v = cnt.processed;
+                }
+                a.per_query[qi].steps = (int64_t)st;
+                a.per_query[qi].nodes_visited = (int64_t)v;
+                a.per_query[qi].nodes_processed = (int64_t)cnt.processed;
+            }
+        }
     }
-    flush_stats<STATS>(a, qi, active, cnt);
+    if (active) add_totals<STATS>(a, cnt.steps, cnt.visited, cnt.processed);
+    else add_totals<STATS>(a, 0, 0, 0);
 }
 
 // Host-side dispatch (walk_dispatch.cu).  Returns the number of launches.

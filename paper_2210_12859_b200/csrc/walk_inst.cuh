@@ -9,19 +9,47 @@ inline unsigned walk_blocks(int64_t m, int threads) {
     return unsigned((m + threads - 1) / threads);
 }
 
+// Persistent grid: every SM filled to its occupancy limit, never more
+// blocks than the work needs.
+template <class K>
+unsigned persistent_blocks(K kernel, int64_t m) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, 0);
+    const int64_t full = int64_t(sms) * (per_sm > 0 ? per_sm : 1);
+    const int64_t need = (m + 255) / 256;
+    return unsigned(need < full ? need : full);
+}
+
+template <int D, int S, int KB, bool STATS, bool UNORDERED>
+void launch_one(const WalkArgs& a, cudaStream_t st) {
+    if constexpr (KB >= 64) {  // 128 list registers: the persistent kernel would spill
+        walk_kernel<D, S, KB, STATS, UNORDERED><<<walk_blocks(a.m, 256), 256, 0, st>>>(a);
+        return;
+    } else if (a.persistent) {
+        auto kern = walk_persistent_kernel<D, S, KB, STATS, UNORDERED>;
+        static const unsigned cap = persistent_blocks(kern, int64_t(1) << 40);
+        const int64_t need = (a.m + 255) / 256;
+        const unsigned grid = unsigned(need < cap ? need : cap);
+        kern<<<grid, 256, 0, st>>>(a);
+    } else {
+        walk_kernel<D, S, KB, STATS, UNORDERED><<<walk_blocks(a.m, 256), 256, 0, st>>>(a);
+    }
+}
+
 template <int D, int S, int KB>
 int launch_bucket(const WalkArgs& a, bool stats, bool unordered, cudaStream_t st) {
-    const unsigned grid = walk_blocks(a.m, 256);
     if (stats) {
         if (unordered)
-            walk_kernel<D, S, KB, true, true><<<grid, 256, 0, st>>>(a);
+            launch_one<D, S, KB, true, true>(a, st);
         else
-            walk_kernel<D, S, KB, true, false><<<grid, 256, 0, st>>>(a);
+            launch_one<D, S, KB, true, false>(a, st);
     } else {
         if (unordered)
-            walk_kernel<D, S, KB, false, true><<<grid, 256, 0, st>>>(a);
+            launch_one<D, S, KB, false, true>(a, st);
         else
-            walk_kernel<D, S, KB, false, false><<<grid, 256, 0, st>>>(a);
+            launch_one<D, S, KB, false, false>(a, st);
     }
     return 1;
 }
