@@ -42,19 +42,21 @@ struct Tuning {
     int persistent = 0;
     int chunk = 64;
     int refill = 8;
+    int budget = 4096;
 };
 
-// Launch tuning, overridable for experiments: FKD_PERSIST=0|1,
-// FKD_WORK_CHUNK=<positions per fetch>, FKD_REFILL=<idle lanes>.
-const Tuning& tuning() {
-    static const Tuning t = [] {
+// Launch tuning, overridable per call for experiments and tests:
+// FKD_PERSIST=0|1, FKD_WORK_CHUNK=<positions per fetch>,
+// FKD_REFILL=<idle lanes>, FKD_BUDGET=<loop trips before the overflow pass>.
+Tuning tuning() {
+    return [] {
         Tuning x;
         if (const char* e = std::getenv("FKD_PERSIST")) x.persistent = std::atoi(e) != 0;
         if (const char* e = std::getenv("FKD_WORK_CHUNK")) x.chunk = std::max(32, std::atoi(e));
         if (const char* e = std::getenv("FKD_REFILL")) x.refill = std::min(32, std::max(1, std::atoi(e)));
+        if (const char* e = std::getenv("FKD_BUDGET")) x.budget = std::max(0, std::atoi(e));
         return x;
     }();
-    return t;
 }
 
 // Store layout: padded vectors (1, 2, 4, 4, 8, 8, 8, 8 floats) by default;
@@ -84,7 +86,9 @@ struct Workspace {
     int64_t key_cap = 0;
     void* sort_tmp = nullptr;
     size_t sort_tmp_bytes = 0;
-    unsigned long long* small = nullptr;    // [8]: bad, steps, visited, processed, work counter
+    unsigned long long* small = nullptr;    // [8]: bad, steps, visited, processed, work, ovf count, ovf next
+    uint32_t* ovf = nullptr;                // overflow query ids
+    int64_t ovf_cap = 0;
     unsigned long long* h_small = nullptr;  // pinned mirror
     // host-path staging
     float* q = nullptr;
@@ -99,6 +103,7 @@ struct Workspace {
         cudaFree(keys);
         cudaFree(ids);
         cudaFree(sort_tmp);
+        cudaFree(ovf);
         cudaFree(small);
         cudaFreeHost(h_small);
         cudaFree(q);
@@ -286,9 +291,18 @@ fkd_status enqueue(const fkd_tree* t, Replica& r, Workspace* w, const float* d_q
         a.bad = w->small;
         a.id_base = base;
         a.work = w->small + 4;
-        a.chunk = tuning().chunk;
-        a.refill = tuning().refill;
-        a.persistent = tuning().persistent;
+        const Tuning tu = tuning();
+        a.chunk = tu.chunk;
+        a.refill = tu.refill;
+        a.persistent = tu.persistent;
+        a.budget = (stats || walk_bucket_of(k) == 0 || t->dim > 8 || a.persistent) ? 0 : tu.budget;
+        if (a.budget > 0) {
+            FKD_CUDA(grow(w->ovf, w->ovf_cap, cm));
+            a.ovf_ids = w->ovf;
+            a.ovf_count = w->small + 5;
+            a.ovf_next = w->small + 6;
+            FKD_CUDA(cudaMemsetAsync(w->small + 5, 0, 2 * sizeof(unsigned long long), st));
+        }
         if (sort) {
             const int64_t half = w->key_cap / 2;
             const int rc = morton_order(a.queries, cm, t->dim, t->frame, w->keys, w->keys + half,
@@ -301,8 +315,9 @@ fkd_status enqueue(const fkd_tree* t, Replica& r, Workspace* w, const float* d_q
         if (a.persistent) FKD_CUDA(cudaMemsetAsync(a.work, 0, sizeof(unsigned long long), st));
         const int nl = launch_walk(a, t->dim, t->stride, stats, (o->flags & FKD_FLAG_UNORDERED) != 0, st);
         if (nl <= 0) return fail(FKD_CUDA_ERROR, "no kernel for this configuration");
-        *launches += nl;
-        *walk_launches += nl;
+        const int tail = a.budget > 0 ? 1 : 0;  // the overflow pass
+        *launches += nl + tail;
+        *walk_launches += nl + tail;
         FKD_CUDA(cudaGetLastError());
     }
     return FKD_OK;

@@ -61,6 +61,10 @@ struct WalkArgs {
     int32_t chunk;              // persistent kernel: positions claimed per fetch
     int32_t refill;             // persistent kernel: idle lanes that trigger a refill
     int32_t persistent;         // launch the persistent lane-refill kernel
+    int32_t budget;             // loop trips before a query moves to the overflow pass (0 = none)
+    uint32_t* ovf_ids;          // [m] ids of queries over budget
+    unsigned long long* ovf_count;
+    unsigned long long* ovf_next;
 };
 
 __device__ __forceinline__ uint64_t make_key(float d2, int32_t node) {
@@ -334,10 +338,23 @@ __global__ void __launch_bounds__(256) walk_kernel(const WalkArgs a) {
     LaneWalk<D, S, KB, STATS, UNORDERED> w;
     bool active = i < a.m && w.init(a, i);
     if (active) {
-        if (a.n > 0)
-            while (w.step(a)) {
+        bool over = false;
+        if (a.n > 0) {
+            if (STATS || a.budget <= 0) {
+                while (w.step(a)) {
+                }
+            } else {
+                int trips = a.budget;
+                while (w.step(a)) {
+                    if (--trips == 0) {
+                        over = true;
+                        break;
+                    }
+                }
             }
-        w.finish(a);
+        }
+        w.finish(a);  // over budget: the partial list stays as the overflow pass's bound
+        if (over) a.ovf_ids[atomicAdd(a.ovf_count, 1ull)] = uint32_t(w.qi);
     }
     if (active) add_totals<STATS>(a, w.cnt.steps, w.cnt.visited, w.cnt.processed);
     else add_totals<STATS>(a, 0, 0, 0);

@@ -1,6 +1,7 @@
 // walk_inst.cuh — explicit instantiation helpers; one translation unit per
 // dimension (walk_d*.cu) so nvcc compiles the kernel matrix in parallel.
 #pragma once
+#include "overflow.cuh"
 #include "walk.cuh"
 
 namespace fkd {
@@ -22,10 +23,22 @@ unsigned persistent_blocks(K kernel, int64_t m) {
     return unsigned(need < full ? need : full);
 }
 
+// Tail pass over the queries the walk kernel stopped (overflow.cuh); a
+// persistent grid reads the device-side overflow count, so no host sync.
+template <int D, int S, int KB>
+void launch_overflow(const WalkArgs& a, cudaStream_t st) {
+    constexpr int T = KB >= 32 ? 256 : 512;
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    overflow_kernel<D, S, KB, T><<<sms, T, 0, st>>>(a);
+}
+
 template <int D, int S, int KB, bool STATS, bool UNORDERED>
 void launch_one(const WalkArgs& a, cudaStream_t st) {
     if constexpr (KB >= 64) {  // 128 list registers: the persistent kernel would spill
         walk_kernel<D, S, KB, STATS, UNORDERED><<<walk_blocks(a.m, 256), 256, 0, st>>>(a);
+        if (!STATS && a.budget > 0) launch_overflow<D, S, KB>(a, st);
         return;
     } else if (a.persistent) {
         auto kern = walk_persistent_kernel<D, S, KB, STATS, UNORDERED>;
@@ -35,6 +48,7 @@ void launch_one(const WalkArgs& a, cudaStream_t st) {
         kern<<<grid, 256, 0, st>>>(a);
     } else {
         walk_kernel<D, S, KB, STATS, UNORDERED><<<walk_blocks(a.m, 256), 256, 0, st>>>(a);
+        if (!STATS && a.budget > 0) launch_overflow<D, S, KB>(a, st);
     }
 }
 

@@ -194,3 +194,42 @@ def test_cpp_shim_against_reference():
     out = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "OK" in out.stdout
+
+
+@pytest.mark.parametrize("budget", ["1", "3", "50"])
+def test_overflow_pass_is_exact(oracle, budget, monkeypatch):
+    """Queries stopped by the walk budget are finished by the CTA-per-query
+    overflow pass (overflow.cuh); results must stay bit-exact."""
+    monkeypatch.setenv("FKD_BUDGET", budget)
+    rng = oracle.instance_rng(777)
+    for t in range(24):
+        n = rng.next_int(1, 6000)
+        dim = rng.next_int(1, 8)
+        grid = 8 if t % 3 == 0 else 0
+        pts = rng.random_point_set(n, dim, grid, 0.2 if t % 2 else 0.0)
+        nodes = oracle.build_tree(pts)
+        qs = np.stack([rng.random_query(dim, pts) for _ in range(300)])
+        tree = fk.KdTree.from_level_order(nodes)
+        for k, r in ((0, INF), (1, 0.25), (4, INF), (8, 0.01), (16, INF), (20, 0.25), (50, INF), (64, 0.0)):
+            res = fk.run_batch(tree, qs, fk.BatchOptions(kind=_kind(k), k=max(k, 1), max_radius=r))
+            ref = oracle.run_batch(nodes, qs, "knn" if k else "fcp", max(k, 1), r)
+            bad = np.nonzero(res.counts != ref[0])[0]
+            kk = max(k, 1)
+            if len(bad) == 0:
+                hb = np.nonzero((res.hits.view(np.uint64) != ref[1].view(np.uint64)).reshape(-1, kk).any(1))[0]
+                bad = hb
+            assert len(bad) == 0, (t, n, dim, k, r, len(bad), bad[:3].tolist(), res.counts[bad[:1]].tolist(),
+                                   ref[0][bad[:1]].tolist(), res.hits.reshape(-1, kk)[bad[:1]].tolist(),
+                                   ref[1].reshape(-1, kk)[bad[:1]].tolist())
+
+
+def test_overflow_clustered_tail(oracle, monkeypatch):
+    monkeypatch.setenv("FKD_BUDGET", "256")
+    pts = fk.clustered_points(3, 1, 200_000, 3)
+    qs = fk.clustered_points(3, 2, 20_000, 3)
+    nodes = fk.build_level_order(pts)
+    tree = fk.KdTree.from_level_order(nodes)
+    for k in (0, 8):
+        res = fk.run_batch(tree, qs, fk.BatchOptions(kind=_kind(k), k=max(k, 1)))
+        c, h, _, _ = oracle.run_batch(nodes, qs, "knn" if k else "fcp", max(k, 1), INF)
+        assert np.array_equal(res.counts, c) and res.hits.tobytes() == h.tobytes()
