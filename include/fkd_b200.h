@@ -82,9 +82,10 @@ typedef struct fkd_batch_options {
  * the launch stream), filled only when the caller passes a non-NULL pointer
  * (adds one stream synchronisation). */
 typedef struct fkd_timings {
-    float order_ms;   /* Morton keys + radix sort (0 when not sorting) */
-    float walk_ms;    /* traversal kernel(s)                           */
-    int32_t launches; /* kernels this library launched for the call    */
+    float order_ms;   /* Morton keys + radix sort (0 when not sorting)          */
+    float walk_ms;    /* traversal kernel(s), overflow pass included             */
+    float tail_ms;    /* of walk_ms: the overflow pass for over-budget queries   */
+    int32_t launches; /* kernels this library launched for the call             */
     int32_t walk_launches;
 } fkd_timings;
 
@@ -121,11 +122,11 @@ fkd_status fkd_run_batch(const fkd_tree* tree, const float* queries, int64_t m, 
                          fkd_query_stats* stats);
 
 /* Device buffers on the tree's first device, launched on `stream` (a
- * cudaStream_t; NULL = legacy default stream).  Asynchronous unless stats,
- * per_query or timings is requested or validation must report an error: the
- * non-finite-query check (batch.cpp:79) is resolved with one synchronisation
- * at the end of the call.  per_query (device, may be NULL) receives each
- * query's counters in input order. */
+ * cudaStream_t; NULL = legacy default stream).  The kernels are enqueued on
+ * `stream`; the call then synchronises that stream once, because the
+ * non-finite-query check (batch.cpp:79) must be reported as a status.
+ * d_hits must be 8-byte aligned.  per_query (device, may be NULL) receives
+ * each query's counters in input order (reference stack-free counting). */
 fkd_status fkd_run_batch_device(const fkd_tree* tree, const float* d_queries, int64_t m,
                                 int32_t dim, const fkd_batch_options* opt, int32_t* d_counts,
                                 fkd_hit* d_hits, fkd_query_stats* stats,

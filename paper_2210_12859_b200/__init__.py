@@ -283,7 +283,7 @@ def run_batch_device(tree: KdTree, queries, counts, hits, options: Optional[Batc
         _stream_ptr(stream), C.byref(tm) if timings else None))
     tdict = None
     if timings:
-        tdict = {"order_ms": tm.order_ms, "walk_ms": tm.walk_ms, "launches": tm.launches,
+        tdict = {"order_ms": tm.order_ms, "walk_ms": tm.walk_ms, "tail_ms": tm.tail_ms, "launches": tm.launches,
                  "walk_launches": tm.walk_launches}
     return QueryStats.from_c(st), tdict
 

@@ -42,7 +42,7 @@ struct Tuning {
     int persistent = 0;
     int chunk = 64;
     int refill = 8;
-    int budget = 4096;
+    int budget = 2048;
 };
 
 // Launch tuning, overridable per call for experiments and tests:
@@ -80,7 +80,7 @@ int store_stride(int dim) {
 struct Workspace {
     int device = 0;
     cudaStream_t stream = nullptr;  // own stream (host path)
-    cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     uint32_t* keys = nullptr;       // [2 * cap] keys in/out
     uint32_t* ids = nullptr;        // [2 * cap] ids in/out
     int64_t key_cap = 0;
@@ -244,7 +244,7 @@ bool use_morton(const fkd_tree* t, const fkd_batch_options* o, int64_t m) {
 fkd_status enqueue(const fkd_tree* t, Replica& r, Workspace* w, const float* d_q, int64_t m,
                    const fkd_batch_options* o, float cap2, int32_t* d_counts, fkd_hit* d_hits,
                    fkd_query_stats* d_per_query, bool stats, cudaStream_t st, int* launches,
-                   int* walk_launches, cudaEvent_t ev_mid) {
+                   int* walk_launches, cudaEvent_t ev_mid, cudaEvent_t ev_tail = nullptr) {
     const int k = o->kind == FKD_KNN ? o->k : 1;
     if (t->n == 0) {  // every query returns empty; queries are not read (batch.cpp:75)
         *launches += fill_empty(d_counts, d_hits, m, k, st);
@@ -313,12 +313,15 @@ fkd_status enqueue(const fkd_tree* t, Replica& r, Workspace* w, const float* d_q
         }
         if (ev_mid && base == 0) FKD_CUDA(cudaEventRecord(ev_mid, st));
         if (a.persistent) FKD_CUDA(cudaMemsetAsync(a.work, 0, sizeof(unsigned long long), st));
-        const int nl = launch_walk(a, t->dim, t->stride, stats, (o->flags & FKD_FLAG_UNORDERED) != 0, st);
+        const bool unordered = (o->flags & FKD_FLAG_UNORDERED) != 0;
+        const int nl = launch_walk(a, t->dim, t->stride, stats, unordered, 0, st);
         if (nl <= 0) return fail(FKD_CUDA_ERROR, "no kernel for this configuration");
-        const int tail = a.budget > 0 ? 1 : 0;  // the overflow pass
+        FKD_CUDA(cudaGetLastError());
+        if (ev_tail && base == 0) FKD_CUDA(cudaEventRecord(ev_tail, st));
+        const int tail = launch_walk(a, t->dim, t->stride, stats, unordered, 1, st);  // overflow pass
+        FKD_CUDA(cudaGetLastError());
         *launches += nl + tail;
         *walk_launches += nl + tail;
-        FKD_CUDA(cudaGetLastError());
     }
     return FKD_OK;
 }
@@ -327,19 +330,19 @@ fkd_status enqueue(const fkd_tree* t, Replica& r, Workspace* w, const float* d_q
 
 int walk_bucket(int k) { return walk_bucket_of(k); }
 
-int launch_walk(const WalkArgs& a, int dim, int stride, bool stats, bool unordered,
+int launch_walk(const WalkArgs& a, int dim, int stride, bool stats, bool unordered, int phase,
                 cudaStream_t st) {
     const int KB = walk_bucket_of(a.k);
-    if (KB == 0 || dim > 8) return launch_walk_heap(a, dim, stats, unordered, st);
+    if (KB == 0 || dim > 8) return phase == 0 ? launch_walk_heap(a, dim, stats, unordered, st) : 0;
     switch (dim) {
-        case 1: return launch_walk_d1(a, stride, KB, stats, unordered, st);
-        case 2: return launch_walk_d2(a, stride, KB, stats, unordered, st);
-        case 3: return launch_walk_d3(a, stride, KB, stats, unordered, st);
-        case 4: return launch_walk_d4(a, stride, KB, stats, unordered, st);
-        case 5: return launch_walk_d5(a, stride, KB, stats, unordered, st);
-        case 6: return launch_walk_d6(a, stride, KB, stats, unordered, st);
-        case 7: return launch_walk_d7(a, stride, KB, stats, unordered, st);
-        case 8: return launch_walk_d8(a, stride, KB, stats, unordered, st);
+        case 1: return launch_walk_d1(a, stride, KB, stats, unordered, phase, st);
+        case 2: return launch_walk_d2(a, stride, KB, stats, unordered, phase, st);
+        case 3: return launch_walk_d3(a, stride, KB, stats, unordered, phase, st);
+        case 4: return launch_walk_d4(a, stride, KB, stats, unordered, phase, st);
+        case 5: return launch_walk_d5(a, stride, KB, stats, unordered, phase, st);
+        case 6: return launch_walk_d6(a, stride, KB, stats, unordered, phase, st);
+        case 7: return launch_walk_d7(a, stride, KB, stats, unordered, phase, st);
+        case 8: return launch_walk_d8(a, stride, KB, stats, unordered, phase, st);
         default: return 0;
     }
 }
@@ -559,7 +562,7 @@ fkd_status fkd_run_batch_device(const fkd_tree* t, const float* d_q, int64_t m, 
     fkd_status s = validate(t, m, dim, o, &cap2);
     if (s != FKD_OK) return s;
     if (stats) *stats = fkd_query_stats{0, 0, 0};
-    if (timings) *timings = fkd_timings{0.0f, 0.0f, 0, 0};
+    if (timings) *timings = fkd_timings{0.0f, 0.0f, 0.0f, 0, 0};
     if (m == 0) return FKD_OK;
     if (t->reps.empty()) return fail(FKD_NO_DEVICE, "tree has no device replica");
     if ((reinterpret_cast<uintptr_t>(d_hits) & 7u) != 0)
@@ -576,7 +579,8 @@ fkd_status fkd_run_batch_device(const fkd_tree* t, const float* d_q, int64_t m, 
         FKD_CUDA(cudaMemcpyAsync(w->small, init, sizeof(init), cudaMemcpyHostToDevice, st));
         if (timings) FKD_CUDA(cudaEventRecord(w->ev[0], st));
         fkd_status e = enqueue(t, r, w, d_q, m, o, cap2, d_counts, d_hits, d_per_query, want_stats,
-                               st, &launches, &walk_launches, timings ? w->ev[1] : nullptr);
+                               st, &launches, &walk_launches, timings ? w->ev[1] : nullptr,
+                               timings ? w->ev[3] : nullptr);
         if (e != FKD_OK) return e;
         if (timings) FKD_CUDA(cudaEventRecord(w->ev[2], st));
         FKD_CUDA(cudaMemcpyAsync(w->h_small, w->small, sizeof(init), cudaMemcpyDeviceToHost, st));
@@ -589,6 +593,7 @@ fkd_status fkd_run_batch_device(const fkd_tree* t, const float* d_q, int64_t m, 
         if (timings) {
             cudaEventElapsedTime(&timings->order_ms, w->ev[0], w->ev[1]);
             cudaEventElapsedTime(&timings->walk_ms, w->ev[1], w->ev[2]);
+            cudaEventElapsedTime(&timings->tail_ms, w->ev[3], w->ev[2]);
             timings->launches = launches;
             timings->walk_launches = walk_launches;
         }

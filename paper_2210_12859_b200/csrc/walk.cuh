@@ -591,8 +591,10 @@ __global__ void __launch_bounds__(128) walk_heap_kernel(const WalkArgs a) {
 }
 
 // Host-side dispatch (walk_dispatch.cu).  Returns the number of launches.
+// phase 0 launches the walk, phase 1 the overflow pass (0 launches when the
+// batch was not budgeted).
 int launch_walk(const WalkArgs& a, int dim, int layout_stride, bool stats, bool unordered,
-                cudaStream_t stream);
+                int phase, cudaStream_t stream);
 
 // Register-list capacity used for k (0 = heap kernel).
 int walk_bucket(int k);

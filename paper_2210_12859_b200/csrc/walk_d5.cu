@@ -1,8 +1,8 @@
 // walk_d5.cu — 5-D kernels over the S=8 store.
 #include "walk_inst.cuh"
 namespace fkd {
-int launch_walk_d5(const WalkArgs& a, int S, int KB, bool stats, bool unordered, cudaStream_t st) {
+int launch_walk_d5(const WalkArgs& a, int S, int KB, bool stats, bool unordered, int phase, cudaStream_t st) {
     (void)S;
-    return launch_fixed<5, 8>(a, KB, stats, unordered, st);
+    return launch_fixed<5, 8>(a, KB, stats, unordered, phase, st);
 }
 }  // namespace fkd

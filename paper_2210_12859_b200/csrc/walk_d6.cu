@@ -1,8 +1,8 @@
 // walk_d6.cu — 6-D kernels over the S=8 store.
 #include "walk_inst.cuh"
 namespace fkd {
-int launch_walk_d6(const WalkArgs& a, int S, int KB, bool stats, bool unordered, cudaStream_t st) {
+int launch_walk_d6(const WalkArgs& a, int S, int KB, bool stats, bool unordered, int phase, cudaStream_t st) {
     (void)S;
-    return launch_fixed<6, 8>(a, KB, stats, unordered, st);
+    return launch_fixed<6, 8>(a, KB, stats, unordered, phase, st);
 }
 }  // namespace fkd

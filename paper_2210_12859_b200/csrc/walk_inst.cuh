@@ -38,8 +38,6 @@ template <int D, int S, int KB, bool STATS, bool UNORDERED>
 void launch_one(const WalkArgs& a, cudaStream_t st) {
     if constexpr (KB >= 64) {  // 128 list registers: the persistent kernel would spill
         walk_kernel<D, S, KB, STATS, UNORDERED><<<walk_blocks(a.m, 256), 256, 0, st>>>(a);
-        if (!STATS && a.budget > 0) launch_overflow<D, S, KB>(a, st);
-        return;
     } else if (a.persistent) {
         auto kern = walk_persistent_kernel<D, S, KB, STATS, UNORDERED>;
         static const unsigned cap = persistent_blocks(kern, int64_t(1) << 40);
@@ -48,12 +46,17 @@ void launch_one(const WalkArgs& a, cudaStream_t st) {
         kern<<<grid, 256, 0, st>>>(a);
     } else {
         walk_kernel<D, S, KB, STATS, UNORDERED><<<walk_blocks(a.m, 256), 256, 0, st>>>(a);
-        if (!STATS && a.budget > 0) launch_overflow<D, S, KB>(a, st);
     }
 }
 
+// phase 0: the walk kernel; phase 1: the overflow pass (when budgeted)
 template <int D, int S, int KB>
-int launch_bucket(const WalkArgs& a, bool stats, bool unordered, cudaStream_t st) {
+int launch_bucket(const WalkArgs& a, bool stats, bool unordered, int phase, cudaStream_t st) {
+    if (phase == 1) {
+        if (stats || a.budget <= 0) return 0;
+        launch_overflow<D, S, KB>(a, st);
+        return 1;
+    }
     if (stats) {
         if (unordered)
             launch_one<D, S, KB, true, true>(a, st);
@@ -69,15 +72,15 @@ int launch_bucket(const WalkArgs& a, bool stats, bool unordered, cudaStream_t st
 }
 
 template <int D, int S>
-int launch_fixed(const WalkArgs& a, int KB, bool stats, bool unordered, cudaStream_t st) {
+int launch_fixed(const WalkArgs& a, int KB, bool stats, bool unordered, int phase, cudaStream_t st) {
     switch (KB) {
-        case 1: return launch_bucket<D, S, 1>(a, stats, unordered, st);
-        case 2: return launch_bucket<D, S, 2>(a, stats, unordered, st);
-        case 4: return launch_bucket<D, S, 4>(a, stats, unordered, st);
-        case 8: return launch_bucket<D, S, 8>(a, stats, unordered, st);
-        case 16: return launch_bucket<D, S, 16>(a, stats, unordered, st);
-        case 32: return launch_bucket<D, S, 32>(a, stats, unordered, st);
-        case 64: return launch_bucket<D, S, 64>(a, stats, unordered, st);
+        case 1: return launch_bucket<D, S, 1>(a, stats, unordered, phase, st);
+        case 2: return launch_bucket<D, S, 2>(a, stats, unordered, phase, st);
+        case 4: return launch_bucket<D, S, 4>(a, stats, unordered, phase, st);
+        case 8: return launch_bucket<D, S, 8>(a, stats, unordered, phase, st);
+        case 16: return launch_bucket<D, S, 16>(a, stats, unordered, phase, st);
+        case 32: return launch_bucket<D, S, 32>(a, stats, unordered, phase, st);
+        case 64: return launch_bucket<D, S, 64>(a, stats, unordered, phase, st);
         default: return 0;
     }
 }
@@ -100,14 +103,14 @@ int launch_heap(const WalkArgs& a, bool stats, bool unordered, cudaStream_t st) 
 }
 
 // per-dimension entry points (defined in walk_d<D>.cu)
-int launch_walk_d1(const WalkArgs&, int S, int KB, bool, bool, cudaStream_t);
-int launch_walk_d2(const WalkArgs&, int S, int KB, bool, bool, cudaStream_t);
-int launch_walk_d3(const WalkArgs&, int S, int KB, bool, bool, cudaStream_t);
-int launch_walk_d4(const WalkArgs&, int S, int KB, bool, bool, cudaStream_t);
-int launch_walk_d5(const WalkArgs&, int S, int KB, bool, bool, cudaStream_t);
-int launch_walk_d6(const WalkArgs&, int S, int KB, bool, bool, cudaStream_t);
-int launch_walk_d7(const WalkArgs&, int S, int KB, bool, bool, cudaStream_t);
-int launch_walk_d8(const WalkArgs&, int S, int KB, bool, bool, cudaStream_t);
+int launch_walk_d1(const WalkArgs&, int S, int KB, bool, bool, int phase, cudaStream_t);
+int launch_walk_d2(const WalkArgs&, int S, int KB, bool, bool, int phase, cudaStream_t);
+int launch_walk_d3(const WalkArgs&, int S, int KB, bool, bool, int phase, cudaStream_t);
+int launch_walk_d4(const WalkArgs&, int S, int KB, bool, bool, int phase, cudaStream_t);
+int launch_walk_d5(const WalkArgs&, int S, int KB, bool, bool, int phase, cudaStream_t);
+int launch_walk_d6(const WalkArgs&, int S, int KB, bool, bool, int phase, cudaStream_t);
+int launch_walk_d7(const WalkArgs&, int S, int KB, bool, bool, int phase, cudaStream_t);
+int launch_walk_d8(const WalkArgs&, int S, int KB, bool, bool, int phase, cudaStream_t);
 int launch_walk_heap(const WalkArgs&, int dim, bool, bool, cudaStream_t);
 
 }  // namespace fkd

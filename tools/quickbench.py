@@ -42,17 +42,18 @@ def main():
         for morton in (True, False):
             opt = fk.BatchOptions(kind=kind, k=k, max_radius=r, morton=morton)
             fk.run_batch_device(tree, dq, counts, hits, opt)
-            walk, order = [], []
+            walk, order, tail = [], [], []
             for _ in range(args.reps):
                 _, tm = fk.run_batch_device(tree, dq, counts, hits, opt, timings=True)
                 walk.append(tm["walk_ms"])
                 order.append(tm["order_ms"])
+                tail.append(tm["tail_ms"])
             st, _ = fk.run_batch_device(tree, dq, counts, hits,
                                         fk.BatchOptions(kind=kind, k=k, max_radius=r, morton=morton,
                                                         collect_stats=True))
             w = float(np.median(walk))
             o = float(np.median(order))
-            print(json.dumps({"cfg": name, "morton": morton, "walk_ms": round(w, 3), "order_ms": round(o, 3),
+            print(json.dumps({"cfg": name, "morton": morton, "walk_ms": round(w, 3), "order_ms": round(o, 3), "tail_ms": round(float(np.median(tail)), 3),
                               "walk_qps": round(args.m / w * 1e3 / 1e6, 1), "total_qps_M": round(args.m / (w + o) * 1e3 / 1e6, 1),
                               "P": st.nodes_processed / args.m, "steps": st.steps / args.m}), flush=True)
 
