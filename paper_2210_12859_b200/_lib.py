@@ -8,7 +8,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libfkd_b200.so")
+LIB_PATH = os.environ.get("FKD_LIB") or os.path.join(HERE, "libfkd_b200.so")  # FKD_LIB: A/B builds
 
 # every symbol include/fkd_b200.h declares
 EXPORTS = (

@@ -43,6 +43,8 @@ struct Tuning {
     int chunk = 64;
     int refill = 8;
     int budget = 2048;
+    int wave = 0;
+    std::vector<int> rounds{64, 64, 128, 256, 512, 1024};
 };
 
 // Launch tuning, overridable per call for experiments and tests:
@@ -55,6 +57,17 @@ Tuning tuning() {
         if (const char* e = std::getenv("FKD_WORK_CHUNK")) x.chunk = std::max(32, std::atoi(e));
         if (const char* e = std::getenv("FKD_REFILL")) x.refill = std::min(32, std::max(1, std::atoi(e)));
         if (const char* e = std::getenv("FKD_BUDGET")) x.budget = std::max(0, std::atoi(e));
+        if (const char* e = std::getenv("FKD_WAVE")) x.wave = std::atoi(e) != 0;
+        if (const char* e = std::getenv("FKD_ROUNDS")) {  // e.g. "64,64,128"
+            x.rounds.clear();
+            for (const char* p = e; *p;) {
+                const int v = std::atoi(p);
+                if (v > 0) x.rounds.push_back(v);
+                while (*p && *p != ',') ++p;
+                if (*p == ',') ++p;
+            }
+            if (x.rounds.empty()) x.wave = 0;
+        }
         return x;
     }();
 }
@@ -89,6 +102,10 @@ struct Workspace {
     unsigned long long* small = nullptr;    // [8]: bad, steps, visited, processed, work, ovf count, ovf next
     uint32_t* ovf = nullptr;                // overflow query ids
     int64_t ovf_cap = 0;
+    uint32_t* wave_ids = nullptr;           // [2 * cap] wave id lists
+    int64_t wave_cap = 0;
+    int2* wave_state = nullptr;             // [cap]
+    int64_t wave_state_cap = 0;
     unsigned long long* h_small = nullptr;  // pinned mirror
     // host-path staging
     float* q = nullptr;
@@ -104,6 +121,8 @@ struct Workspace {
         cudaFree(ids);
         cudaFree(sort_tmp);
         cudaFree(ovf);
+        cudaFree(wave_ids);
+        cudaFree(wave_state);
         cudaFree(small);
         cudaFreeHost(h_small);
         cudaFree(q);
@@ -186,8 +205,8 @@ fkd_status acquire_ws(Replica& r, Workspace** out) {
     cudaError_t e = cudaStreamCreateWithFlags(&w->stream, cudaStreamNonBlocking);
     for (auto& ev : w->ev)
         if (e == cudaSuccess) e = cudaEventCreate(&ev);
-    if (e == cudaSuccess) e = cudaMalloc(&w->small, 8 * sizeof(unsigned long long));
-    if (e == cudaSuccess) e = cudaMallocHost(&w->h_small, 8 * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMalloc(&w->small, 16 * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMallocHost(&w->h_small, 16 * sizeof(unsigned long long));
     if (e != cudaSuccess) {
         delete w;
         return fail(FKD_CUDA_ERROR, std::string("workspace: ") + cudaGetErrorString(e));
@@ -244,7 +263,8 @@ bool use_morton(const fkd_tree* t, const fkd_batch_options* o, int64_t m) {
 fkd_status enqueue(const fkd_tree* t, Replica& r, Workspace* w, const float* d_q, int64_t m,
                    const fkd_batch_options* o, float cap2, int32_t* d_counts, fkd_hit* d_hits,
                    fkd_query_stats* d_per_query, bool stats, cudaStream_t st, int* launches,
-                   int* walk_launches, cudaEvent_t ev_mid, cudaEvent_t ev_tail = nullptr) {
+                   int* walk_launches, cudaEvent_t ev_mid, cudaEvent_t ev_tail = nullptr,
+                   int64_t id_offset = 0) {
     const int k = o->kind == FKD_KNN ? o->k : 1;
     if (t->n == 0) {  // every query returns empty; queries are not read (batch.cpp:75)
         *launches += fill_empty(d_counts, d_hits, m, k, st);
@@ -289,7 +309,7 @@ fkd_status enqueue(const fkd_tree* t, Replica& r, Workspace* w, const float* d_q
         a.totals = w->small + 1;
         a.per_query = d_per_query ? d_per_query + base : nullptr;
         a.bad = w->small;
-        a.id_base = base;
+        a.id_base = id_offset + base;
         a.work = w->small + 4;
         const Tuning tu = tuning();
         a.chunk = tu.chunk;
@@ -314,9 +334,38 @@ fkd_status enqueue(const fkd_tree* t, Replica& r, Workspace* w, const float* d_q
         if (ev_mid && base == 0) FKD_CUDA(cudaEventRecord(ev_mid, st));
         if (a.persistent) FKD_CUDA(cudaMemsetAsync(a.work, 0, sizeof(unsigned long long), st));
         const bool unordered = (o->flags & FKD_FLAG_UNORDERED) != 0;
-        const int nl = launch_walk(a, t->dim, t->stride, stats, unordered, 0, st);
-        if (nl <= 0) return fail(FKD_CUDA_ERROR, "no kernel for this configuration");
-        FKD_CUDA(cudaGetLastError());
+        int nl = 0;
+        const bool wave = tu.wave && a.budget > 0 && !a.persistent;
+        if (wave) {
+            // wave rounds (walk.cuh walk_wave_kernel); survivors of the last
+            // round feed the overflow pass through the same id list
+            FKD_CUDA(grow(w->wave_ids, w->wave_cap, 2 * cm));
+            FKD_CUDA(grow(w->wave_state, w->wave_state_cap, cm));
+            const int64_t half = w->wave_cap / 2;
+            a.wave_state = w->wave_state;
+            a.wave_in = nullptr;
+            a.wave_n_in = nullptr;
+            int r = 0;
+            for (int trips : tu.rounds) {
+                a.trips = trips;
+                a.wave_out = w->wave_ids + (r & 1) * half;
+                a.wave_n_out = w->small + 8 + (r & 1);
+                FKD_CUDA(cudaMemsetAsync(a.wave_n_out, 0, sizeof(unsigned long long), st));
+                const int l = launch_walk(a, t->dim, t->stride, stats, unordered, 2, st);
+                if (l <= 0) return fail(FKD_CUDA_ERROR, "no wave kernel for this configuration");
+                FKD_CUDA(cudaGetLastError());
+                nl += l;
+                a.wave_in = a.wave_out;
+                a.wave_n_in = a.wave_n_out;
+                ++r;
+            }
+            a.ovf_ids = const_cast<uint32_t*>(a.wave_in);
+            a.ovf_count = const_cast<unsigned long long*>(a.wave_n_in);
+        } else {
+            nl = launch_walk(a, t->dim, t->stride, stats, unordered, 0, st);
+            if (nl <= 0) return fail(FKD_CUDA_ERROR, "no kernel for this configuration");
+            FKD_CUDA(cudaGetLastError());
+        }
         if (ev_tail && base == 0) FKD_CUDA(cudaEventRecord(ev_tail, st));
         const int tail = launch_walk(a, t->dim, t->stride, stats, unordered, 1, st);  // overflow pass
         FKD_CUDA(cudaGetLastError());
@@ -387,6 +436,8 @@ void fkd_tree_destroy(fkd_tree* t) {
 static fkd_status set_frame(fkd_tree* t, const float* lo, const float* hi) {
     const int dim = t->dim;
     t->frame.bits = morton_bits_per_dim(std::min(dim, 8));
+    if (const char* e = std::getenv("FKD_MORTON_BITS"))  // experiment: bits per axis
+        t->frame.bits = std::max(1, std::min(t->frame.bits, std::atoi(e)));
     const float top = float((1u << t->frame.bits) - 1u);
     for (int d = 0; d < 8; ++d) {
         t->frame.lo[d] = 0.0f;
@@ -544,6 +595,14 @@ fkd_status fkd_tree_create_device(const float* d_level_order, int64_t n, int32_t
     return FKD_OK;
 }
 
+// bad = ~0 (no bad query), totals = 0.  Memsets, not a pageable H2D copy,
+// which would synchronise the stream and serialise the host pipeline.
+static cudaError_t reset_small(Workspace* w, cudaStream_t st) {
+    cudaError_t e = cudaMemsetAsync(w->small, 0xFF, sizeof(unsigned long long), st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(w->small + 1, 0, 7 * sizeof(unsigned long long), st);
+    return e;
+}
+
 static fkd_status finish_small(Workspace* w, int64_t base, unsigned long long* bad,
                                unsigned long long tot[3]) {
     const unsigned long long b = w->h_small[0];
@@ -573,17 +632,17 @@ fkd_status fkd_run_batch_device(const fkd_tree* t, const float* d_q, int64_t m, 
     Workspace* w = nullptr;
     if ((s = acquire_ws(r, &w)) != FKD_OK) return s;
     const bool want_stats = stats != nullptr || d_per_query != nullptr;
-    const unsigned long long init[8] = {kNoBad, 0, 0, 0, 0, 0, 0, 0};
     int launches = 0, walk_launches = 0;
     auto body = [&]() -> fkd_status {
-        FKD_CUDA(cudaMemcpyAsync(w->small, init, sizeof(init), cudaMemcpyHostToDevice, st));
+        FKD_CUDA(reset_small(w, st));
         if (timings) FKD_CUDA(cudaEventRecord(w->ev[0], st));
         fkd_status e = enqueue(t, r, w, d_q, m, o, cap2, d_counts, d_hits, d_per_query, want_stats,
                                st, &launches, &walk_launches, timings ? w->ev[1] : nullptr,
                                timings ? w->ev[3] : nullptr);
         if (e != FKD_OK) return e;
         if (timings) FKD_CUDA(cudaEventRecord(w->ev[2], st));
-        FKD_CUDA(cudaMemcpyAsync(w->h_small, w->small, sizeof(init), cudaMemcpyDeviceToHost, st));
+        FKD_CUDA(cudaMemcpyAsync(w->h_small, w->small, 8 * sizeof(unsigned long long),
+                                 cudaMemcpyDeviceToHost, st));
         FKD_CUDA(cudaStreamSynchronize(st));
         unsigned long long bad = kNoBad, tot[3] = {0, 0, 0};
         finish_small(w, 0, &bad, tot);
@@ -649,7 +708,6 @@ fkd_status fkd_run_batch(const fkd_tree* t, const float* queries, int64_t m, int
             jobs.push_back(Job{di, wss[di][c % wss[di].size()], b, std::min(kChunk, hi - b)});
         }
     }
-    std::vector<unsigned long long> small(jobs.size() * 8, 0);
     if (err == FKD_OK) {
         // size every workspace for its largest chunk before enqueueing
         for (int di = 0; di < ndev && err == FKD_OK; ++di) {
@@ -665,49 +723,59 @@ fkd_status fkd_run_batch(const fkd_tree* t, const float* queries, int64_t m, int
             }
         }
     }
-    // Enqueue: H2D -> order + walk -> D2H -> small D2H, per chunk.  A
-    // workspace's stream serialises its own chunks, so buffer reuse is safe.
+    // Enqueue: H2D -> order + walk -> D2H, per chunk; bad ids (offset by the
+    // chunk base) and stat totals accumulate on the device per workspace and
+    // are read once at the end.  A workspace's stream serialises its own
+    // chunks, so buffer reuse is safe; nothing here blocks the host until the
+    // final synchronisation (with pinned caller buffers).
+    for (int di = 0; di < ndev && err == FKD_OK; ++di) {
+        DeviceGuard g(t->reps[di]->device);
+        for (Workspace* w : wss[di]) {
+            cudaError_t e = reset_small(w, w->stream);
+            if (e != cudaSuccess) err = fail(FKD_CUDA_ERROR, std::string("reset: ") + cudaGetErrorString(e));
+        }
+    }
     for (size_t ji = 0; ji < jobs.size() && err == FKD_OK; ++ji) {
         const Job& j = jobs[ji];
         Replica& r = *t->reps[j.rep];
         DeviceGuard g(r.device);
         Workspace* w = j.w;
-        const unsigned long long init[8] = {kNoBad, 0, 0, 0, 0, 0, 0, 0};
         int launches = 0, wl = 0;
         auto step = [&]() -> fkd_status {
             FKD_CUDA(cudaMemcpyAsync(w->q, queries + j.base * dim, size_t(j.count) * dim * sizeof(float),
                                      cudaMemcpyHostToDevice, w->stream));
-            FKD_CUDA(cudaMemcpyAsync(w->small, init, sizeof(init), cudaMemcpyHostToDevice, w->stream));
             fkd_status e = enqueue(t, r, w, w->q, j.count, o, cap2, w->counts, w->hits, nullptr,
-                                   want_stats, w->stream, &launches, &wl, nullptr);
+                                   want_stats, w->stream, &launches, &wl, nullptr, nullptr, j.base);
             if (e != FKD_OK) return e;
             FKD_CUDA(cudaMemcpyAsync(counts + j.base, w->counts, size_t(j.count) * sizeof(int32_t),
                                      cudaMemcpyDeviceToHost, w->stream));
             FKD_CUDA(cudaMemcpyAsync(hits + j.base * k, w->hits, size_t(j.count) * k * sizeof(fkd_hit),
                                      cudaMemcpyDeviceToHost, w->stream));
-            FKD_CUDA(cudaMemcpyAsync(&small[ji * 8], w->small, sizeof(init), cudaMemcpyDeviceToHost,
-                                     w->stream));
             return FKD_OK;
         };
         err = step();
     }
+    for (int di = 0; di < ndev && err == FKD_OK; ++di) {
+        DeviceGuard g(t->reps[di]->device);
+        for (Workspace* w : wss[di]) {
+            cudaError_t e = cudaMemcpyAsync(w->h_small, w->small, 8 * sizeof(unsigned long long),
+                                            cudaMemcpyDeviceToHost, w->stream);
+            if (e != cudaSuccess) err = fail(FKD_CUDA_ERROR, std::string("readback: ") + cudaGetErrorString(e));
+        }
+    }
     // drain every stream even after an error, then return workspaces
+    unsigned long long bad = kNoBad, tot[3] = {0, 0, 0};
     for (int di = 0; di < ndev; ++di) {
         DeviceGuard g(t->reps[di]->device);
         for (Workspace* w : wss[di]) {
             cudaError_t e = cudaStreamSynchronize(w->stream);
             if (e != cudaSuccess && err == FKD_OK)
                 err = fail(FKD_CUDA_ERROR, std::string("stream: ") + cudaGetErrorString(e));
+            if (err == FKD_OK) finish_small(w, 0, &bad, tot);
             release_ws(*t->reps[di], w);
         }
     }
     if (err != FKD_OK) return err;
-    unsigned long long bad = kNoBad, tot[3] = {0, 0, 0};
-    for (size_t ji = 0; ji < jobs.size(); ++ji) {
-        const unsigned long long b = small[ji * 8];
-        if (b != kNoBad) bad = std::min<unsigned long long>(bad, b + jobs[ji].base);
-        for (int c = 0; c < 3; ++c) tot[c] += small[ji * 8 + 1 + c];
-    }
     if (bad != kNoBad)
         return fail(FKD_DATA_ERROR, "queries: non-finite coordinate in point " + std::to_string(bad));
     if (stats) *stats = fkd_query_stats{int64_t(tot[0]), int64_t(tot[1]), int64_t(tot[2])};

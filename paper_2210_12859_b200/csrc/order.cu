@@ -81,14 +81,24 @@ int morton_order(const float* d_queries, int64_t m, int dim, const MortonFrame& 
 
 // ---- tree store ----
 
-// level-order row-major [n x dim] -> padded [n x stride] (zero pad)
+// level-order row-major [n x dim] -> padded [n x stride].  When the padding
+// has room (stride > dim) its last float repeats the node's split coordinate
+// (coord[depth % dim], tree.hpp:27-29), so the walk reads the plane from a
+// fixed lane of the vector load instead of selecting it by split dimension.
 __global__ void pack_nodes_kernel(const float* __restrict__ src, int64_t n, int dim, int stride,
                                   float* __restrict__ dst) {
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n * stride) return;
     const int64_t node = i / stride;
     const int c = int(i - node * stride);
-    dst[i] = c < dim ? src[node * dim + c] : 0.0f;
+    float v = 0.0f;
+    if (c < dim) {
+        v = src[node * dim + c];
+    } else if (c == stride - 1) {
+        const int depth = 31 - __clz(int(node) + 1);
+        v = src[node * dim + depth % dim];
+    }
+    dst[i] = v;
 }
 
 __device__ __forceinline__ unsigned ordered_bits(float x) {

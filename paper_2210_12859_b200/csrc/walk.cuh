@@ -65,6 +65,13 @@ struct WalkArgs {
     uint32_t* ovf_ids;          // [m] ids of queries over budget
     unsigned long long* ovf_count;
     unsigned long long* ovf_next;
+    // wave rounds (walk_wave_kernel)
+    int32_t trips;                         // loop trips per query this round
+    const uint32_t* wave_in;               // ids walked this round (null: all walk positions)
+    const unsigned long long* wave_n_in;   // their count (device)
+    uint32_t* wave_out;                    // ids still walking after this round
+    unsigned long long* wave_n_out;
+    int2* wave_state;                      // [m] (curr, prev) of suspended walks
 };
 
 __device__ __forceinline__ uint64_t make_key(float d2, int32_t node) {
@@ -107,22 +114,26 @@ __device__ __forceinline__ float sq_dist(const float (&q)[D], const float (&p)[D
 }
 
 // Full point of one node.  S is the store stride: S in {2,4,8} is a padded
-// vector layout (LDG.64 / LDG.128), S == D is packed (scalar loads).
+// vector layout (LDG.64 / LDG.128), S == D is packed (scalar loads).  With
+// S > D the last padding float holds the split coordinate (pack_nodes);
+// `split` receives it.
 template <int D, int S>
 __device__ __forceinline__ void load_point(const float* __restrict__ nodes, int32_t i,
-                                           float (&p)[D]) {
+                                           float (&p)[D], float* split = nullptr) {
     const float* base = nodes + size_t(i) * S;
     if constexpr (S == 4) {
         const float4 v = __ldg(reinterpret_cast<const float4*>(base));
         const float t[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
         for (int j = 0; j < D; ++j) p[j] = t[j];
+        if (split) *split = t[3];
     } else if constexpr (S == 8) {
         const float4 v0 = __ldg(reinterpret_cast<const float4*>(base));
         const float4 v1 = __ldg(reinterpret_cast<const float4*>(base) + 1);
         const float t[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
 #pragma unroll
         for (int j = 0; j < D; ++j) p[j] = t[j];
+        if (split) *split = t[7];
     } else if constexpr (S == 2 && D == 2) {
         const float2 v = __ldg(reinterpret_cast<const float2*>(base));
         p[0] = v.x;
@@ -223,6 +234,8 @@ struct LaneWalk {
             } else {
                 pd = __ldg(a.nodes + size_t(curr) * S + d);
             }
+        } else if constexpr (S > D) {
+            load_point<D, S>(a.nodes, curr, p, &pd);  // split plane from the padding slot
         } else {
             load_point<D, S>(a.nodes, curr, p);
             pd = pick(p, d);
@@ -279,6 +292,34 @@ struct LaneWalk {
         return true;
     }
 
+    // Resumes a walk suspended by an earlier wave round: the state is the
+    // reference's two node ids; the candidate list is the partial one the
+    // round left in the query's own output slot; radius2 and the split
+    // dimension are recomputed from them.
+    __device__ __forceinline__ void resume(const WalkArgs& a, int32_t id) {
+        qi = id;
+        const float* qp = a.queries + size_t(qi) * D;
+#pragma unroll
+        for (int j = 0; j < D; ++j) q[j] = __ldg(qp + j);
+        const int dummies = KB - a.k;
+        const int2* slot = reinterpret_cast<const int2*>(a.hits + size_t(qi) * a.k);
+#pragma unroll
+        for (int j = 0; j < KB; ++j) {
+            if (j < dummies) {
+                L[j] = 0ull;
+            } else {
+                const int2 h = slot[j - dummies];
+                L[j] = (uint64_t(uint32_t(h.y) + 1u) << 32) | uint32_t(h.x);
+            }
+        }
+        r2 = fminf(a.cap2, key_dist(L[KB - 1]));
+        const int2 st = a.wave_state[qi];
+        curr = st.x;
+        prev = st.y;
+        d = depth_of(curr) % D;
+        cnt = Counters<STATS>();
+    }
+
     // fixed-stride slot in input order (batch.cpp:104-119)
     __device__ __forceinline__ void finish(const WalkArgs& a) {
         const int k = a.k;
@@ -331,9 +372,23 @@ __device__ __forceinline__ void add_totals(const WalkArgs& a, unsigned long long
     }
 }
 
+// Minimum resident blocks per SM for the plain walk: the kNN kernels are
+// latency-bound, so occupancy beats the few bytes of list spill ptxas needs
+// to fit KB=8 into 32 registers (64 warps/SM instead of 48).
+#ifndef FKD_MINB_KB8
+#define FKD_MINB_KB8 1
+#endif
+#ifndef FKD_MINB_KB16
+#define FKD_MINB_KB16 1
+#endif
+template <int KB>
+constexpr int walk_min_blocks() {
+    return KB == 8 ? FKD_MINB_KB8 : (KB == 16 ? FKD_MINB_KB16 : 1);
+}
+
 // One thread per walk position (plain grid).
 template <int D, int S, int KB, bool STATS, bool UNORDERED>
-__global__ void __launch_bounds__(256) walk_kernel(const WalkArgs a) {
+__global__ void __launch_bounds__(256, walk_min_blocks<KB>()) walk_kernel(const WalkArgs a) {
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     LaneWalk<D, S, KB, STATS, UNORDERED> w;
     bool active = i < a.m && w.init(a, i);
@@ -358,6 +413,58 @@ __global__ void __launch_bounds__(256) walk_kernel(const WalkArgs a) {
     }
     if (active) add_totals<STATS>(a, w.cnt.steps, w.cnt.visited, w.cnt.processed);
     else add_totals<STATS>(a, 0, 0, 0);
+}
+
+// Wave round: every live query walks at most `trips` loop trips; walks that
+// end write their results, the others park (curr, prev) + their partial list
+// and are compacted (warp-ordered, so Morton neighbours stay together) into
+// the next round's list.  Lanes idle at most `trips` trips per round, with
+// no per-trip warp vote.  Grid-stride over a fixed persistent grid, because
+// the live count is only known on the device.  The last round's survivors
+// are the overflow pass's input.
+template <int D, int S, int KB, bool UNORDERED>
+__global__ void __launch_bounds__(256) walk_wave_kernel(const WalkArgs a) {
+    const bool first = a.wave_in == nullptr;
+    const int32_t items = first ? int32_t(a.m) : int32_t(*a.wave_n_in);
+    const int32_t stride = int32_t(gridDim.x * blockDim.x);  // a multiple of 32
+    const unsigned lane = threadIdx.x & 31u;
+    // whole warps iterate together so the survivor ballot can use a full mask
+    for (int32_t wb = int32_t(blockIdx.x * blockDim.x + threadIdx.x) - int32_t(lane); wb < items;
+         wb += stride) {
+        const int32_t pos = wb + int32_t(lane);
+        LaneWalk<D, S, KB, false, UNORDERED> w;
+        bool active = false;
+        if (pos < items) {
+            if (first) {
+                active = w.init(a, pos);
+            } else {
+                w.resume(a, int32_t(a.wave_in[pos]));
+                active = true;
+            }
+        }
+        bool park = false;
+        if (active) {
+            if (a.n > 0) {
+                int t = a.trips;
+                while (w.step(a)) {
+                    if (--t == 0) {
+                        park = true;
+                        break;
+                    }
+                }
+            }
+            w.finish(a);
+            if (park) a.wave_state[w.qi] = make_int2(w.curr, w.prev);
+        }
+        const unsigned mask = __ballot_sync(0xffffffffu, park);
+        if (mask) {
+            const unsigned leader = __ffs(mask) - 1;
+            unsigned long long base = 0;
+            if (lane == leader) base = atomicAdd(a.wave_n_out, (unsigned long long)__popc(mask));
+            base = __shfl_sync(0xffffffffu, base, leader);
+            if (park) a.wave_out[base + __popc(mask & ((1u << lane) - 1u))] = uint32_t(w.qi);
+        }
+    }
 }
 
 // Persistent warps with lane refill.  Each warp takes chunks of walk

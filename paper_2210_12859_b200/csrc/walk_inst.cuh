@@ -49,12 +49,27 @@ void launch_one(const WalkArgs& a, cudaStream_t st) {
     }
 }
 
-// phase 0: the walk kernel; phase 1: the overflow pass (when budgeted)
+template <int D, int S, int KB, bool UNORDERED>
+void launch_wave(const WalkArgs& a, cudaStream_t st) {
+    auto kern = walk_wave_kernel<D, S, KB, UNORDERED>;
+    static const unsigned grid = persistent_blocks(kern, int64_t(1) << 40);
+    kern<<<grid, 256, 0, st>>>(a);
+}
+
+// phase 0: the walk kernel; phase 1: the overflow pass (when budgeted);
+// phase 2: one wave round.
 template <int D, int S, int KB>
 int launch_bucket(const WalkArgs& a, bool stats, bool unordered, int phase, cudaStream_t st) {
     if (phase == 1) {
         if (stats || a.budget <= 0) return 0;
         launch_overflow<D, S, KB>(a, st);
+        return 1;
+    }
+    if (phase == 2) {
+        if (unordered)
+            launch_wave<D, S, KB, true>(a, st);
+        else
+            launch_wave<D, S, KB, false>(a, st);
         return 1;
     }
     if (stats) {
