@@ -20,7 +20,7 @@ namespace fkd {
 
 int morton_bits_per_dim(int dim) {
     if (dim <= 0) return 0;
-    int b = 30 / dim;
+    int b = 24 / dim;  // 24-bit keys: three 8-bit onesweep passes (measured: no walk cost vs 30 bits)
     if (b > 16) b = 16;
     if (b < 1) b = 1;
     return b;

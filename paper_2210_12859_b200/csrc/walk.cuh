@@ -186,7 +186,12 @@ __device__ __forceinline__ int dim_down(int d) {  // split dim one level up
 
 template <int D, int S, int KB, bool STATS, bool UNORDERED>
 struct LaneWalk {
+    // With a split-plane slot in the store (S > D) the walk never needs the
+    // split dimension: qr holds the query rotated so that qr[0] is the
+    // coordinate split at the current depth (rotated by one per level).
+    static constexpr bool kRot = S > D && D > 1;
     float q[D];
+    float qr[kRot ? D : 1];
     uint64_t L[KB];
     int32_t curr, prev;
     int d;  // split dim of curr, tracked incrementally (tree.hpp:27-29)
@@ -208,6 +213,10 @@ struct LaneWalk {
         if (!finite) {
             atomicMin(a.bad, (unsigned long long)(a.id_base + qi));
             return false;
+        }
+        if constexpr (kRot) {
+#pragma unroll
+            for (int j = 0; j < D; ++j) qr[j] = q[j];  // depth 0 splits dim 0
         }
         const int dummies = KB - a.k;
 #pragma unroll
@@ -250,7 +259,12 @@ struct LaneWalk {
         }
         cnt.step(1, 1, from_parent ? 1 : 0);
 
-        const float sd = __fsub_rn(pick(q, d), pd);                // 226
+        float qd;
+        if constexpr (kRot)
+            qd = qr[0];
+        else
+            qd = pick(q, d);
+        const float sd = __fsub_rn(qd, pd);                         // 226
         const int cs = sd > 0.0f;                                  // 227
         const bool fir = __fmul_rn(sd, sd) <= r2;                  // 230
         const int32_t parent = ((curr + 1) >> 1) - 1;              // 205
@@ -286,7 +300,16 @@ struct LaneWalk {
             }
         }
         if (next < 0) return false;  // 240-244
-        d = next == parent ? dim_down<D>(d) : dim_up<D>(d);
+        if constexpr (kRot) {
+            const bool up = next == parent;
+            float t[D];
+#pragma unroll
+            for (int j = 0; j < D; ++j) t[j] = up ? qr[(j + D - 1) % D] : qr[(j + 1) % D];
+#pragma unroll
+            for (int j = 0; j < D; ++j) qr[j] = t[j];
+        } else {
+            d = next == parent ? dim_down<D>(d) : dim_up<D>(d);
+        }
         prev = curr;
         curr = next;
         return true;
@@ -317,6 +340,10 @@ struct LaneWalk {
         curr = st.x;
         prev = st.y;
         d = depth_of(curr) % D;
+        if constexpr (kRot) {
+#pragma unroll
+            for (int j = 0; j < D; ++j) qr[j] = q[(d + j) % D];
+        }
         cnt = Counters<STATS>();
     }
 
