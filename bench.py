@@ -229,8 +229,14 @@ def run_b200(args) -> None:
     desc, n, m, dim, gkind, batches = WORKLOADS[args.workload]
 
     # ---- tree: built on rank 0, replicated by NCCL broadcast
-    nodes_host = fk.build_level_order(gen_points(fk, gkind, 1, n, dim)) if rank == 0 else None
-    nodes_dev = replicate_tree(nodes_host, n, dim, dev)
+    # GPU build on rank 0 (csrc/build.cu, byte-identical to flatkd::build_tree)
+    if rank == 0:
+        nodes_dev = fk.build_level_order_device(torch.from_numpy(gen_points(fk, gkind, 1, n, dim)).to(dev))
+        nodes_host = nodes_dev.cpu().numpy()
+    else:
+        nodes_host = None
+        nodes_dev = None
+    nodes_dev = replicate_tree(nodes_host, n, dim, dev) if world > 1 else nodes_dev
     tree = fk.KdTree.from_device(nodes_dev)
 
     qs_host = gen_points(fk, gkind, query_stream(rank), m, dim)

@@ -149,6 +149,19 @@ fkd_status fkd_knn(const fkd_tree* tree, const float* query, int32_t dim, int32_
  * byte-identical to the reference's. */
 fkd_status fkd_build_tree(const float* points, int64_t n, int32_t dim, float* level_order_out);
 
+/* The same build on the GPU: device points in, device
+ * level-order array out, byte-identical to flatkd::build_tree.  Rejects
+ * non-finite points ("build: non-finite coordinate in point i"). */
+fkd_status fkd_build_tree_device(const float* d_points, int64_t n, int32_t dim,
+                                 float* d_level_order_out, void* stream);
+
+/* Host points -> GPU build on the first device -> tree store on every listed
+ * device (build_tree + KdTree::from_level_order in one call, no host
+ * round trip of the level-order array).  level_order_out (host, may be NULL)
+ * receives the array. */
+fkd_status fkd_tree_build(const float* points, int64_t n, int32_t dim, const int32_t* devices,
+                          int32_t ndev, float* level_order_out, fkd_tree** out);
+
 /* BatchResult::result_hash (batch.cpp:30-48). */
 uint64_t fkd_result_hash(const int32_t* counts, const fkd_hit* hits, int64_t m, int32_t stride);
 

@@ -40,7 +40,7 @@ from ._lib import LIB, LIB_PATH, fkd_batch_options, fkd_query_stats, fkd_timings
 __all__ = [
     "BatchOptions", "BatchResult", "DataError", "DeviceError", "Engine", "HIT_DTYPE",
     "InvalidArgument", "InvariantError", "KdTree", "QueryKind", "QueryStats", "build_tree",
-    "clustered_points", "fcp", "knn", "random_points", "result_hash", "run_batch",
+    "build_level_order", "build_level_order_device", "clustered_points", "fcp", "knn", "random_points", "result_hash", "run_batch",
     "run_batch_device", "write_query_results", "LIB_PATH",
 ]
 
@@ -220,12 +220,39 @@ class KdTree:
 
 
 def build_tree(points, devices: Optional[Sequence[int]] = None) -> KdTree:
-    """flatkd::build_tree (tree.cpp:80-89) + upload: the unique left-balanced tree."""
-    return KdTree.from_level_order(build_level_order(points), devices)
+    """flatkd::build_tree (tree.cpp:80-89) on the GPU (csrc/build.cu) + the
+    device tree store: the unique left-balanced tree, byte-identical to the
+    reference's.  ``tree.nodes()`` holds the level-order array."""
+    arr = _f32(points)
+    if arr.ndim != 2:
+        raise DataError("point set: expected an (n, dim) array")
+    n, dim = arr.shape
+    out = np.empty_like(arr)
+    h = C.c_void_p()
+    devs = (C.c_int32 * len(devices))(*devices) if devices else None
+    _check(LIB.fkd_tree_build(arr.ctypes.data, n, dim, devs, len(devices) if devices else 0,
+                              out.ctypes.data, C.byref(h)))
+    return KdTree(h, n, dim, out)
+
+
+def build_level_order_device(points, out=None, stream=None):
+    """GPU build from a CUDA float32 (n, dim) tensor; returns the level-order
+    tensor (``out`` if given)."""
+    import torch
+
+    if not points.is_cuda or points.dtype != torch.float32 or points.dim() != 2:
+        raise DataError("expected a CUDA float32 (n, dim) tensor")
+    p = points.contiguous()
+    if out is None:
+        out = torch.empty_like(p)
+    _check(LIB.fkd_build_tree_device(C.c_void_p(p.data_ptr()), p.shape[0], p.shape[1],
+                                     C.c_void_p(out.data_ptr()), _stream_ptr(stream)))
+    return out
 
 
 def build_level_order(points) -> np.ndarray:
-    """Host builder only: the reference's level-order array (byte-identical)."""
+    """Host (multi-threaded CPU) builder: the reference's level-order array
+    (byte-identical).  Needs no GPU; for large sets prefer build_tree()."""
     arr = _f32(points)
     if arr.ndim != 2:
         raise DataError("point set: expected an (n, dim) array")

@@ -14,7 +14,7 @@ LIB_PATH = os.environ.get("FKD_LIB") or os.path.join(HERE, "libfkd_b200.so")  # 
 EXPORTS = (
     "fkd_default_options", "fkd_tree_create", "fkd_tree_create_device", "fkd_tree_destroy",
     "fkd_tree_size", "fkd_tree_dim", "fkd_run_batch", "fkd_run_batch_device", "fkd_fcp", "fkd_knn",
-    "fkd_build_tree", "fkd_result_hash", "fkd_random_points", "fkd_clustered_points",
+    "fkd_build_tree", "fkd_build_tree_device", "fkd_tree_build", "fkd_result_hash", "fkd_random_points", "fkd_clustered_points",
     "fkd_host_alloc", "fkd_host_free", "fkd_last_error", "fkd_version",
 )
 
@@ -56,6 +56,8 @@ def _load() -> C.CDLL:
     lib.fkd_fcp.argtypes = [vp, vp, i32, C.c_float, vp, vp, vp]
     lib.fkd_knn.argtypes = [vp, vp, i32, i32, C.c_float, vp, vp, vp]
     lib.fkd_build_tree.argtypes = [vp, i64, i32, vp]
+    lib.fkd_build_tree_device.argtypes = [vp, i64, i32, vp, vp]
+    lib.fkd_tree_build.argtypes = [vp, i64, i32, vp, i32, vp, vp]
     lib.fkd_result_hash.restype = C.c_uint64
     lib.fkd_result_hash.argtypes = [vp, vp, i64, i32]
     lib.fkd_random_points.argtypes = [C.c_uint64, C.c_uint64, i64, i32, vp]

@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "fkd_b200.h"
+#include "build.cuh"
 #include "order.cuh"
 #include "walk.cuh"
 #include "walk_inst.cuh"
@@ -611,6 +612,68 @@ static fkd_status finish_small(Workspace* w, int64_t base, unsigned long long* b
     tot[1] += w->h_small[2];
     tot[2] += w->h_small[3];
     return FKD_OK;
+}
+
+fkd_status fkd_build_tree_device(const float* d_points, int64_t n, int32_t dim, float* d_out,
+                                 void* stream) {
+    if (n < 0 || n > int64_t(0x7fffffff)) return fail(FKD_DATA_ERROR, "build: size out of range");
+    if (n == 0) return FKD_OK;
+    if (dim < 1) return fail(FKD_DATA_ERROR, "build: dimension must be >= 1");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    // require_finite(points, "build") (tree.cpp:81), on the device
+    unsigned* d_lohi = nullptr;
+    unsigned long long* d_bad = nullptr;
+    unsigned long long bad = kNoBad;
+    FKD_CUDA(cudaMalloc(&d_lohi, 16 * sizeof(unsigned)));
+    FKD_CUDA(cudaMalloc(&d_bad, sizeof(unsigned long long)));
+    FKD_CUDA(cudaMemsetAsync(d_bad, 0xFF, sizeof(unsigned long long), st));
+    FKD_CUDA(cudaMemsetAsync(d_lohi, 0, 16 * sizeof(unsigned), st));
+    tree_scan(d_points, n, dim, d_lohi, d_bad, st);
+    FKD_CUDA(cudaGetLastError());
+    FKD_CUDA(cudaMemcpyAsync(&bad, d_bad, sizeof(bad), cudaMemcpyDeviceToHost, st));
+    FKD_CUDA(cudaStreamSynchronize(st));
+    cudaFree(d_lohi);
+    cudaFree(d_bad);
+    if (bad != kNoBad) return fail(FKD_DATA_ERROR, "build: non-finite coordinate in point " + std::to_string(bad));
+    const BuildStatus bs = build_tree_device(d_points, n, dim, d_out, st);
+    if (bs.err != cudaSuccess) return fail(FKD_CUDA_ERROR, std::string("build: ") + bs.what + ": " + cudaGetErrorString(bs.err));
+    FKD_CUDA(cudaStreamSynchronize(st));
+    return FKD_OK;
+}
+
+fkd_status fkd_tree_build(const float* points, int64_t n, int32_t dim, const int32_t* devices,
+                          int32_t ndev, float* level_order_out, fkd_tree** out) {
+    if (!out) return fail(FKD_INVALID_ARGUMENT, "null output");
+    *out = nullptr;
+    if (n < 0 || n > int64_t(0x7fffffff)) return fail(FKD_DATA_ERROR, "build: size out of range");
+    if (n > 0 && (dim < 1 || !points)) return fail(FKD_DATA_ERROR, "build: bad point set");
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+        return fail(FKD_NO_DEVICE, "no CUDA device visible (the B200 path has no CPU fallback)");
+    int dev0 = 0;
+    if (devices && ndev > 0) dev0 = devices[0]; else cudaGetDevice(&dev0);
+    if (dev0 < 0 || dev0 >= count) return fail(FKD_INVALID_ARGUMENT, "device id out of range");
+    std::vector<float> nodes(size_t(n) * size_t(std::max(dim, 1)));
+    {
+        DeviceGuard g(dev0);
+        float *d_pts = nullptr, *d_out = nullptr;
+        const size_t bytes = size_t(n) * size_t(std::max(dim, 1)) * sizeof(float);
+        if (n > 0) {
+            FKD_CUDA(cudaMalloc(&d_pts, bytes));
+            FKD_CUDA(cudaMalloc(&d_out, bytes));
+            FKD_CUDA(cudaMemcpy(d_pts, points, bytes, cudaMemcpyHostToDevice));
+        }
+        fkd_status s = fkd_build_tree_device(d_pts, n, dim, d_out, nullptr);
+        if (s == FKD_OK && n > 0) {
+            cudaError_t e = cudaMemcpy(nodes.data(), d_out, bytes, cudaMemcpyDeviceToHost);
+            if (e != cudaSuccess) s = fail(FKD_CUDA_ERROR, std::string("build readback: ") + cudaGetErrorString(e));
+        }
+        cudaFree(d_pts);
+        cudaFree(d_out);
+        if (s != FKD_OK) return s;
+    }
+    if (level_order_out && n > 0) std::copy(nodes.begin(), nodes.end(), level_order_out);
+    return fkd_tree_create(nodes.data(), n, dim, devices, ndev, out);
 }
 
 fkd_status fkd_run_batch_device(const fkd_tree* t, const float* d_q, int64_t m, int32_t dim,

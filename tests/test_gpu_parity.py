@@ -233,3 +233,34 @@ def test_overflow_clustered_tail(oracle, monkeypatch):
         res = fk.run_batch(tree, qs, fk.BatchOptions(kind=_kind(k), k=max(k, 1)))
         c, h, _, _ = oracle.run_batch(nodes, qs, "knn" if k else "fcp", max(k, 1), INF)
         assert np.array_equal(res.counts, c) and res.hits.tobytes() == h.tobytes()
+
+
+def test_gpu_builder_byte_identical(oracle):
+    """csrc/build.cu vs the reference builder restated (tree.cpp:55-89)."""
+    import torch
+
+    rng = oracle.instance_rng(31337)
+    cases = [(0, 3), (1, 1), (2, 2), (7, 3), (100, 4), (1000, 3), (4097, 2), (30000, 3), (20000, 8), (5000, 11)]
+    for n, dim in cases:
+        pts = oracle.random_points(n + dim, n, dim)
+        tree = fk.build_tree(pts)
+        assert np.array_equal(tree.nodes(), oracle.build_tree(pts)), (n, dim)
+    for t in range(40):  # ties: grid snapping, duplicates, signed zeros
+        n = rng.next_int(1, 5000)
+        dim = rng.next_int(1, 5)
+        pts = rng.random_point_set(n, dim, (8, 16, 2)[t % 3], 0.3 if t % 2 else 0.0)
+        if t % 4 == 0:
+            pts = pts - np.float32(0.5)
+            pts[rng.next_int(0, n - 1)] = -0.0
+        want = oracle.build_tree(pts)
+        got = fk.build_level_order_device(torch.from_numpy(pts).cuda()).cpu().numpy()
+        assert got.tobytes() == want.tobytes(), (t, n, dim)
+    with pytest.raises(fk.DataError, match="build: non-finite coordinate in point 3"):
+        bad = oracle.random_points(1, 10, 3)
+        bad[3, 1] = np.inf
+        fk.build_tree(bad)
+
+
+def test_gpu_builder_c1_scale():
+    data = fk.random_points(1, 1, 1_000_000, 3)
+    assert np.array_equal(fk.build_tree(data).nodes(), fk.build_level_order(data))
