@@ -142,6 +142,29 @@ fkd_status fkd_knn(const fkd_tree* tree, const float* query, int32_t dim, int32_
                    float max_radius, fkd_hit* out_hits, int32_t* out_count,
                    fkd_query_stats* stats);
 
+/* ---- device trace (traverse.hpp:56-68) ----
+ * Walks m host queries with the literal state machine on the GPU and returns,
+ * per query, its hits (stride k, or 1 for fcp), count, QueryStats and the
+ * event list the reference's Trace records: node id for "processed", ~node
+ * for "bounced" (events[i*cap ...], lens[i] = full length, may exceed cap).
+ * A debugging aid: slow by design (no bounce folding, no Morton order). */
+fkd_status fkd_trace_batch(const fkd_tree* tree, const float* queries, int32_t m, int32_t dim,
+                           int32_t kind, int32_t k, float max_radius, int32_t* counts,
+                           fkd_hit* hits, fkd_query_stats* stats, int32_t* events, int64_t cap,
+                           int64_t* lens);
+
+/* ---- FKDT / FKDX binary files (io.hpp:10-18, io.cpp:50-99) ----
+ * kind 0 = points ("FKDT"), 1 = level-order tree ("FKDX").  Point files may
+ * exceed the reference's INT_MAX-floats limit (up to 2^40 points). */
+fkd_status fkd_file_info(const char* path, int32_t kind, int64_t* count, int32_t* dim);
+/* Streams the payload into device memory d_out (capacity in points) through a
+ * pinned double buffer, then checks finiteness on the device. */
+fkd_status fkd_read_file_device(const char* path, int32_t kind, float* d_out, int64_t capacity_points,
+                                int64_t* count, int32_t* dim, void* stream);
+fkd_status fkd_write_file(const char* path, int32_t kind, const float* data, int64_t count, int32_t dim);
+/* io::read_tree + KdTree::from_level_order straight onto the device(s). */
+fkd_status fkd_tree_load(const char* path, const int32_t* devices, int32_t ndev, fkd_tree** out);
+
 /* ---- host utilities around the path ---- */
 
 /* flatkd::build_tree (tree.cpp:80-89), round-robin policy: the unique

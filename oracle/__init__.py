@@ -248,6 +248,9 @@ class Reference:
         L.fkr_structure_suite.restype = C.c_longlong
         L.fkr_structure_suite.argtypes = [C.c_int, C.c_int, C.POINTER(C.c_longlong)]
         L.fkr_hardware_threads.restype = C.c_int
+        L.fkr_write_file.argtypes = [C.c_char_p, C.c_int, _f32p, C.c_longlong, C.c_int]
+        L.fkr_read_file.argtypes = [C.c_char_p, C.c_int, _f32p, C.c_longlong, C.POINTER(C.c_longlong),
+                                    C.POINTER(C.c_int)]
         L.fkr_layout.argtypes = [C.POINTER(C.c_int)]
 
     def _check(self, rc: int):
@@ -256,6 +259,18 @@ class Reference:
 
     def last_error(self) -> str:
         return self.lib.fkr_last_error().decode()
+
+    def write_file(self, path: str, points, tree: bool = False) -> None:
+        pts = np.ascontiguousarray(points, np.float32)
+        self._check(self.lib.fkr_write_file(path.encode(), int(tree), pts.reshape(-1) if pts.size else
+                                            np.zeros(1, np.float32), pts.shape[0], pts.shape[1]))
+
+    def read_file(self, path: str, tree: bool = False, cap_floats: int = 1 << 26) -> np.ndarray:
+        out = np.empty(cap_floats, np.float32)
+        n = C.c_longlong(0)
+        d = C.c_int(0)
+        self._check(self.lib.fkr_read_file(path.encode(), int(tree), out, cap_floats, C.byref(n), C.byref(d)))
+        return out[: n.value * d.value].reshape(n.value, d.value)
 
     def hardware_threads(self) -> int:
         return self.lib.fkr_hardware_threads()

@@ -24,6 +24,7 @@
 
 #include "flatkd/batch.hpp"
 #include "flatkd/error.hpp"
+#include "flatkd/io.hpp"
 #include "flatkd/rng.hpp"
 #include "flatkd/testing/instancegen.hpp"
 #include "flatkd/testing/oracle.hpp"
@@ -239,6 +240,26 @@ int fkr_random_query(void* r, int dim, const float* points, int n, float* out) {
         auto pts = make_points(points, n, dim);
         auto q = flatkd::testing::random_query(*static_cast<flatkd::testing::InstanceRng*>(r), dim, pts);
         std::memcpy(out, q.data(), q.size() * sizeof(float));
+    });
+}
+
+// io::write_points / write_tree (binary) and io::read_points / read_tree.
+int fkr_write_file(const char* path, int tree, const float* data, long long n, int dim) {
+    return guarded([&] {
+        auto pts = make_points(data, n, dim);
+        if (tree)
+            flatkd::io::write_tree(path, flatkd::KdTree::from_level_order(pts), flatkd::io::Format::binary);
+        else
+            flatkd::io::write_points(path, pts, flatkd::io::Format::binary);
+    });
+}
+
+int fkr_read_file(const char* path, int tree, float* out, long long cap_floats, long long* n, int* dim) {
+    return guarded([&] {
+        flatkd::PointSet p = tree ? flatkd::io::read_tree(path).nodes() : flatkd::io::read_points(path);
+        *n = p.size();
+        *dim = p.dim();
+        if ((long long)p.raw().size() <= cap_floats) std::memcpy(out, p.raw().data(), p.raw().size() * 4);
     });
 }
 

@@ -388,3 +388,57 @@ def clustered_points(seed: int, stream: int, count: int, dim: int, blobs: int = 
     _check(LIB.fkd_clustered_points(seed, stream, count, dim, blobs, C.c_float(sigma),
                                     out.ctypes.data))
     return out.reshape(count, dim)
+
+
+# ---------------------------------------------------------------- debugging
+
+STATS_DTYPE = np.dtype([("steps", "<i8"), ("nodes_visited", "<i8"), ("nodes_processed", "<i8")])
+
+
+def trace(tree: KdTree, queries, kind: QueryKind = QueryKind.fcp, k: int = 1,
+          max_radius: float = INF, cap: int = 4096):
+    """Device trace of each query's walk (traverse.hpp:56-68): returns
+    (counts, hits, stats, events) where events[i] lists node ids processed
+    (>= 0) and ~node for bounces, exactly as flatkd's Trace records them."""
+    q = _f32(queries, tree.dim())
+    m, dim = q.shape
+    kk = int(k) if kind == QueryKind.knn else 1
+    counts = np.zeros(m, np.int32)
+    hits = np.empty(m * kk, HIT_DTYPE)
+    stats = np.zeros(m, STATS_DTYPE)
+    ev = np.zeros(max(m * cap, 1), np.int32)
+    lens = np.zeros(m, np.int64)
+    _check(LIB.fkd_trace_batch(tree.handle, q.ctypes.data, m, dim, int(kind), int(k), C.c_float(max_radius),
+                               counts.ctypes.data, hits.ctypes.data, stats.ctypes.data, ev.ctypes.data,
+                               cap, lens.ctypes.data))
+    events = [ev[i * cap: i * cap + min(int(lens[i]), cap)].copy() for i in range(m)]
+    return counts, hits, stats, events
+
+
+# ---------------------------------------------------------------- files
+
+def write_points_file(path: str, points, tree: bool = False) -> None:
+    """io::write_points / write_tree, binary format (io.cpp:50-99)."""
+    arr = _f32(points)
+    _check(LIB.fkd_write_file(path.encode(), int(tree), arr.ctypes.data, arr.shape[0], arr.shape[1]))
+
+
+def read_points_file_device(path: str, tree: bool = False, device=None):
+    """Binary points/tree file straight into a CUDA tensor (no host copy)."""
+    import torch
+
+    n = C.c_int64(0)
+    d = C.c_int32(0)
+    _check(LIB.fkd_file_info(path.encode(), int(tree), C.byref(n), C.byref(d)))
+    out = torch.empty((n.value, d.value), dtype=torch.float32, device=device or "cuda")
+    _check(LIB.fkd_read_file_device(path.encode(), int(tree), C.c_void_p(out.data_ptr()), n.value,
+                                    C.byref(n), C.byref(d), None))
+    return out
+
+
+def load_tree(path: str, devices: Optional[Sequence[int]] = None) -> KdTree:
+    """io::read_tree + KdTree::from_level_order onto the device(s)."""
+    h = C.c_void_p()
+    devs = (C.c_int32 * len(devices))(*devices) if devices else None
+    _check(LIB.fkd_tree_load(path.encode(), devs, len(devices) if devices else 0, C.byref(h)))
+    return KdTree(h, int(LIB.fkd_tree_size(h)), int(LIB.fkd_tree_dim(h)), None)

@@ -15,7 +15,8 @@ EXPORTS = (
     "fkd_default_options", "fkd_tree_create", "fkd_tree_create_device", "fkd_tree_destroy",
     "fkd_tree_size", "fkd_tree_dim", "fkd_run_batch", "fkd_run_batch_device", "fkd_fcp", "fkd_knn",
     "fkd_build_tree", "fkd_build_tree_device", "fkd_tree_build", "fkd_result_hash", "fkd_random_points", "fkd_clustered_points",
-    "fkd_host_alloc", "fkd_host_free", "fkd_last_error", "fkd_version",
+    "fkd_host_alloc", "fkd_host_free", "fkd_last_error", "fkd_version", "fkd_trace_batch",
+    "fkd_file_info", "fkd_read_file_device", "fkd_write_file", "fkd_tree_load",
 )
 
 
@@ -62,6 +63,11 @@ def _load() -> C.CDLL:
     lib.fkd_result_hash.argtypes = [vp, vp, i64, i32]
     lib.fkd_random_points.argtypes = [C.c_uint64, C.c_uint64, i64, i32, vp]
     lib.fkd_clustered_points.argtypes = [C.c_uint64, C.c_uint64, i64, i32, i32, C.c_float, vp]
+    lib.fkd_trace_batch.argtypes = [vp, vp, i32, i32, i32, i32, C.c_float, vp, vp, vp, vp, i64, vp]
+    lib.fkd_file_info.argtypes = [C.c_char_p, i32, vp, vp]
+    lib.fkd_read_file_device.argtypes = [C.c_char_p, i32, vp, i64, vp, vp, vp]
+    lib.fkd_write_file.argtypes = [C.c_char_p, i32, vp, i64, i32]
+    lib.fkd_tree_load.argtypes = [C.c_char_p, vp, i32, vp]
     lib.fkd_host_alloc.restype = vp
     lib.fkd_host_alloc.argtypes = [C.c_size_t]
     lib.fkd_host_free.argtypes = [vp]

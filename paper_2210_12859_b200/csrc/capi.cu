@@ -17,6 +17,7 @@
 #include "fkd_b200.h"
 #include "build.cuh"
 #include "order.cuh"
+#include "trace.cuh"
 #include "walk.cuh"
 #include "walk_inst.cuh"
 
@@ -843,6 +844,59 @@ fkd_status fkd_run_batch(const fkd_tree* t, const float* queries, int64_t m, int
         return fail(FKD_DATA_ERROR, "queries: non-finite coordinate in point " + std::to_string(bad));
     if (stats) *stats = fkd_query_stats{int64_t(tot[0]), int64_t(tot[1]), int64_t(tot[2])};
     return FKD_OK;
+}
+
+fkd_status fkd_trace_batch(const fkd_tree* t, const float* queries, int32_t m, int32_t dim,
+                           int32_t kind, int32_t k, float max_radius, int32_t* counts, fkd_hit* hits,
+                           fkd_query_stats* stats, int32_t* events, int64_t cap, int64_t* lens) {
+    fkd_batch_options o;
+    fkd_default_options(&o);
+    o.kind = kind;
+    o.k = k;
+    o.max_radius = max_radius;
+    float cap2 = 0.0f;
+    fkd_status s = validate(t, m, dim, &o, &cap2);
+    if (s != FKD_OK) return s;
+    if (m == 0) return FKD_OK;
+    if (cap < 0) return fail(FKD_INVALID_ARGUMENT, "negative trace capacity");
+    for (int64_t i = 0; t->n > 0 && i < int64_t(m) * dim; ++i)
+        if (!std::isfinite(queries[i]))
+            return fail(FKD_DATA_ERROR, "queries: non-finite coordinate in point " + std::to_string(i / dim));
+    const int kk = kind == FKD_KNN ? k : 1;
+    Replica& r = *t->reps[0];
+    DeviceGuard g(r.device);
+    float* dq = nullptr;
+    int32_t *dc = nullptr, *dev = nullptr;
+    fkd_hit* dh = nullptr;
+    fkd_query_stats* ds = nullptr;
+    int64_t* dl = nullptr;
+    auto body = [&]() -> fkd_status {
+        FKD_CUDA(cudaMalloc(&dq, size_t(m) * dim * sizeof(float)));
+        FKD_CUDA(cudaMalloc(&dc, size_t(m) * sizeof(int32_t)));
+        FKD_CUDA(cudaMalloc(&dh, size_t(m) * kk * sizeof(fkd_hit)));
+        FKD_CUDA(cudaMalloc(&ds, size_t(m) * sizeof(fkd_query_stats)));
+        FKD_CUDA(cudaMalloc(&dev, size_t(std::max<int64_t>(1, m * cap)) * sizeof(int32_t)));
+        FKD_CUDA(cudaMalloc(&dl, size_t(m) * sizeof(int64_t)));
+        FKD_CUDA(cudaMemcpy(dq, queries, size_t(m) * dim * sizeof(float), cudaMemcpyHostToDevice));
+        launch_trace(r.nodes, int32_t(t->n), t->dim, t->stride, dq, m, cap2, kk, dc, dh, ds, dev, cap, dl,
+                     nullptr);
+        FKD_CUDA(cudaGetLastError());
+        FKD_CUDA(cudaMemcpy(counts, dc, size_t(m) * sizeof(int32_t), cudaMemcpyDeviceToHost));
+        FKD_CUDA(cudaMemcpy(hits, dh, size_t(m) * kk * sizeof(fkd_hit), cudaMemcpyDeviceToHost));
+        if (stats) FKD_CUDA(cudaMemcpy(stats, ds, size_t(m) * sizeof(fkd_query_stats), cudaMemcpyDeviceToHost));
+        if (events && cap > 0)
+            FKD_CUDA(cudaMemcpy(events, dev, size_t(m) * cap * sizeof(int32_t), cudaMemcpyDeviceToHost));
+        if (lens) FKD_CUDA(cudaMemcpy(lens, dl, size_t(m) * sizeof(int64_t), cudaMemcpyDeviceToHost));
+        return FKD_OK;
+    };
+    s = body();
+    cudaFree(dq);
+    cudaFree(dc);
+    cudaFree(dh);
+    cudaFree(ds);
+    cudaFree(dev);
+    cudaFree(dl);
+    return s;
 }
 
 static fkd_status single(const fkd_tree* t, const float* q, int32_t dim, int kind, int32_t k,

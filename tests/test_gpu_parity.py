@@ -264,3 +264,56 @@ def test_gpu_builder_byte_identical(oracle):
 def test_gpu_builder_c1_scale():
     data = fk.random_points(1, 1, 1_000_000, 3)
     assert np.array_equal(fk.build_tree(data).nodes(), fk.build_level_order(data))
+
+
+def test_device_trace_matches_reference_trace(oracle):
+    """fkd_trace_batch (trace.cu) records the reference's Trace event list
+    (traverse.hpp:56-68, 206-222) and QueryStats, per query."""
+    rng = oracle.instance_rng(55)
+    for t in range(30):
+        n = rng.next_int(0, 800)
+        dim = rng.next_int(1, 5)
+        pts = rng.random_point_set(n, dim, 8 if t % 2 else 0, 0.2)
+        nodes = oracle.build_tree(pts) if n else pts.reshape(0, dim)
+        qs = np.stack([rng.random_query(dim, pts) for _ in range(20)])
+        tree = fk.KdTree.from_level_order(nodes)
+        for kind, k, r in ((fk.QueryKind.fcp, 1, INF), (fk.QueryKind.knn, 5, 0.25), (fk.QueryKind.knn, 70, INF)):
+            counts, hits, stats, events = fk.trace(tree, qs, kind, k, r, cap=20000)
+            stride = k if kind == fk.QueryKind.knn else 1
+            for i, q in enumerate(qs):
+                h, st, tr = oracle.query(nodes, q, "knn" if kind == fk.QueryKind.knn else "fcp", k, r,
+                                         trace_cap=20000)
+                assert counts[i] == len(h)
+                assert hits[i * stride: i * stride + len(h)].tobytes() == h.tobytes()
+                assert tuple(stats[i]) == (int(st["steps"]), int(st["nodes_visited"]), int(st["nodes_processed"]))
+                assert np.array_equal(events[i], tr), (t, i)
+
+
+def test_binary_files_round_trip_with_reference(oracle, reference, tmp_path):
+    import torch
+
+    pts = oracle.random_points(3, 5000, 3)
+    nodes = oracle.build_tree(pts)
+    p1, p2, p3 = str(tmp_path / "a.fkdt"), str(tmp_path / "b.fkdx"), str(tmp_path / "c.fkdt")
+    reference.write_file(p1, pts)                       # reference writer -> our device reader
+    reference.write_file(p2, nodes, tree=True)
+    assert np.array_equal(fk.read_points_file_device(p1).cpu().numpy(), pts)
+    tree = fk.load_tree(p2)
+    assert tree.size() == 5000 and tree.dim() == 3
+    qs = oracle.random_points(4, 1000, 3)
+    res = fk.run_batch(tree, qs, fk.BatchOptions(kind=fk.QueryKind.knn, k=4))
+    c, h, _, _ = oracle.run_batch(nodes, qs, "knn", 4)
+    assert res.hits.tobytes() == h.tobytes()
+    fk.write_points_file(p3, pts)                       # our writer: byte-identical to the reference's
+    assert open(p3, "rb").read() == open(p1, "rb").read()
+    with pytest.raises(fk.DataError, match="file has magic FKDX, expected FKDT"):
+        fk.read_points_file_device(p2)
+    bad = pts.copy()
+    bad[17, 2] = np.nan
+    fk.write_points_file(p3, bad)
+    with pytest.raises(fk.DataError, match="non-finite coordinate in point 17"):
+        fk.read_points_file_device(p3)
+    with open(p3, "wb") as f:
+        f.write(b"FKDT" + (1).to_bytes(4, "little") + (3).to_bytes(4, "little") + (5000).to_bytes(8, "little"))
+    with pytest.raises(fk.DataError, match="payload size does not match header"):
+        fk.read_points_file_device(p3)
