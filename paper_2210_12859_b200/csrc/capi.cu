@@ -744,9 +744,13 @@ fkd_status fkd_run_batch(const fkd_tree* t, const float* queries, int64_t m, int
     const bool want_stats = o->collect_stats != 0;
     const int ndev = int(t->reps.size());
     const int64_t per_dev = (m + ndev - 1) / ndev;
-    static const int64_t kChunk = [] {
-        const char* e = std::getenv("FKD_CHUNK");
-        return e ? std::max<int64_t>(1024, std::atoll(e)) : int64_t(2) << 20;
+    // Chunking: about 8 chunks per device shard (so the first H2D and the
+    // last D2H, which cannot overlap anything, are short), 0.5M..4M queries
+    // each; three workspaces (streams) per device keep the H2D engine, the
+    // SMs and the D2H engine busy at once.  FKD_CHUNK overrides.
+    const int64_t kChunk = [&] {
+        if (const char* e = std::getenv("FKD_CHUNK")) return std::max<int64_t>(1024, std::atoll(e));
+        return std::min<int64_t>(int64_t(4) << 20, std::max<int64_t>(int64_t(512) << 10, (per_dev + 7) / 8));
     }();
 
     struct Job {
@@ -761,7 +765,7 @@ fkd_status fkd_run_batch(const fkd_tree* t, const float* queries, int64_t m, int
         const int64_t lo = std::min<int64_t>(m, di * per_dev), hi = std::min<int64_t>(m, lo + per_dev);
         if (hi <= lo) continue;
         const int64_t nchunks = (hi - lo + kChunk - 1) / kChunk;
-        const int nws = nchunks > 1 ? 2 : 1;
+        const int nws = int(std::min<int64_t>(nchunks, 3));
         for (int j = 0; j < nws && err == FKD_OK; ++j) {
             Workspace* w = nullptr;
             err = acquire_ws(*t->reps[di], &w);

@@ -82,6 +82,16 @@ __device__ __forceinline__ float key_dist(uint64_t key) {
     return __uint_as_float(uint32_t(key >> 32) - 1u);
 }
 
+// Empty slot of a register list: the admission cap's own key with node
+// 0xFFFFFFFF.  Every admissible candidate (d2 <= cap2, inclusive,
+// traverse.hpp:92/122) has a smaller key and every inadmissible one a larger
+// key, so admission is the single compare key < L[KB-1], and radius2 is just
+// key_dist(L[KB-1]): cap2 while the list is short, the kth distance once it
+// is full (traverse.hpp:97, 135-137).  With cap2 = +inf this is kEmptyKey.
+__device__ __forceinline__ uint64_t cap_key(float cap2) {
+    return (uint64_t(__float_as_uint(cap2) + 1u) << 32) | 0xFFFFFFFFull;
+}
+
 __device__ __forceinline__ int32_t depth_of(int32_t node) {  // tree.hpp:20-22
     return 31 - __clz(node + 1);
 }
@@ -219,8 +229,9 @@ struct LaneWalk {
             for (int j = 0; j < D; ++j) qr[j] = q[j];  // depth 0 splits dim 0
         }
         const int dummies = KB - a.k;
+        const uint64_t empty = cap_key(a.cap2);
 #pragma unroll
-        for (int j = 0; j < KB; ++j) L[j] = j < dummies ? 0ull : kEmptyKey;
+        for (int j = 0; j < KB; ++j) L[j] = j < dummies ? 0ull : empty;
         curr = 0;
         prev = -1;
         d = 0;
@@ -252,9 +263,9 @@ struct LaneWalk {
         if (from_parent) {  // traverse.hpp:217-222
             const float d2 = sq_dist(q, p);
             const uint64_t key = make_key(d2, curr);
-            if (d2 <= a.cap2 && key < L[KB - 1]) {
+            if (key < L[KB - 1]) {  // d2 <= cap2 and beats the kth (cap_key)
                 list_insert(L, key);
-                r2 = fminf(a.cap2, key_dist(L[KB - 1]));
+                r2 = key_dist(L[KB - 1]);
             }
         }
         cnt.step(1, 1, from_parent ? 1 : 0);
@@ -325,6 +336,7 @@ struct LaneWalk {
 #pragma unroll
         for (int j = 0; j < D; ++j) q[j] = __ldg(qp + j);
         const int dummies = KB - a.k;
+        const uint64_t empty = cap_key(a.cap2);
         const int2* slot = reinterpret_cast<const int2*>(a.hits + size_t(qi) * a.k);
 #pragma unroll
         for (int j = 0; j < KB; ++j) {
@@ -332,10 +344,10 @@ struct LaneWalk {
                 L[j] = 0ull;
             } else {
                 const int2 h = slot[j - dummies];
-                L[j] = (uint64_t(uint32_t(h.y) + 1u) << 32) | uint32_t(h.x);
+                L[j] = h.x < 0 ? empty : (uint64_t(uint32_t(h.y) + 1u) << 32) | uint32_t(h.x);
             }
         }
-        r2 = fminf(a.cap2, key_dist(L[KB - 1]));
+        r2 = key_dist(L[KB - 1]);
         const int2 st = a.wave_state[qi];
         curr = st.x;
         prev = st.y;
@@ -358,8 +370,10 @@ struct LaneWalk {
             const int s = j - dummies;
             if (s >= 0) {
                 const uint64_t key = L[j];
-                out[s] = make_int2(int32_t(uint32_t(key)), int32_t(uint32_t(key >> 32) - 1u));
-                c += uint32_t(key) != 0xFFFFFFFFu;
+                const bool hit = uint32_t(key) != 0xFFFFFFFFu;  // empty slot -> Hit{-1, +inf}
+                out[s] = make_int2(int32_t(uint32_t(key)),
+                                   hit ? int32_t(uint32_t(key >> 32) - 1u) : 0x7f800000);
+                c += hit;
             }
         }
         a.counts[qi] = c;
