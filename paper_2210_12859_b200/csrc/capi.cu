@@ -47,6 +47,7 @@ struct Tuning {
     int budget = 2048;
     int wave = 0;
     std::vector<int> rounds{64, 64, 128, 256, 512, 1024};
+    int64_t resume_min = 0;  // 0: SMs x 2048
 };
 
 // Launch tuning, overridable per call for experiments and tests:
@@ -60,6 +61,7 @@ Tuning tuning() {
         if (const char* e = std::getenv("FKD_REFILL")) x.refill = std::min(32, std::max(1, std::atoi(e)));
         if (const char* e = std::getenv("FKD_BUDGET")) x.budget = std::max(0, std::atoi(e));
         if (const char* e = std::getenv("FKD_WAVE")) x.wave = std::atoi(e) != 0;
+        if (const char* e = std::getenv("FKD_RESUME_MIN")) x.resume_min = std::atoll(e);
         if (const char* e = std::getenv("FKD_ROUNDS")) {  // e.g. "64,64,128"
             x.rounds.clear();
             for (const char* p = e; *p;) {
@@ -320,10 +322,18 @@ fkd_status enqueue(const fkd_tree* t, Replica& r, Workspace* w, const float* d_q
         a.budget = (stats || walk_bucket_of(k) == 0 || t->dim > 8 || a.persistent) ? 0 : tu.budget;
         if (a.budget > 0) {
             FKD_CUDA(grow(w->ovf, w->ovf_cap, cm));
+            FKD_CUDA(grow(w->wave_state, w->wave_state_cap, cm));
+            FKD_CUDA(grow(w->wave_ids, w->wave_cap, 2 * cm));
             a.ovf_ids = w->ovf;
             a.ovf_count = w->small + 5;
             a.ovf_next = w->small + 6;
+            a.wave_state = w->wave_state;
             FKD_CUDA(cudaMemsetAsync(w->small + 5, 0, 2 * sizeof(unsigned long long), st));
+            // a GPU-full of over-budget queries is bulk work, not a tail
+            int dev = 0, sms = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            a.resume_min = tu.resume_min > 0 ? tu.resume_min : int64_t(sms) * 2048;
         }
         if (sort) {
             const int64_t half = w->key_cap / 2;
@@ -367,6 +377,18 @@ fkd_status enqueue(const fkd_tree* t, Replica& r, Workspace* w, const float* d_q
             nl = launch_walk(a, t->dim, t->stride, stats, unordered, 0, st);
             if (nl <= 0) return fail(FKD_CUDA_ERROR, "no kernel for this configuration");
             FKD_CUDA(cudaGetLastError());
+            if (a.budget > 0) {
+                // resume pass: continues the parked walks with the plain grid
+                // when at least resume_min overflowed (decided on the device)
+                WalkArgs r = a;
+                r.trips = 0x7fffffff;
+                r.wave_in = a.ovf_ids;
+                r.wave_n_in = a.ovf_count;
+                r.wave_out = w->wave_ids;
+                r.wave_n_out = w->small + 8;
+                nl += launch_walk(r, t->dim, t->stride, stats, unordered, 2, st);
+                FKD_CUDA(cudaGetLastError());
+            }
         }
         if (ev_tail && base == 0) FKD_CUDA(cudaEventRecord(ev_tail, st));
         const int tail = launch_walk(a, t->dim, t->stride, stats, unordered, 1, st);  // overflow pass

@@ -67,6 +67,8 @@ __global__ void __launch_bounds__(THREADS) overflow_kernel(const WalkArgs a) {
     const int dummies = KB - k;
     const float cap2 = a.cap2;
 
+    // many over-budget queries were finished by the resume pass instead
+    if (a.resume_min > 0 && *a.ovf_count >= (unsigned long long)a.resume_min) return;
     while (true) {
         if (tid == 0) slot = atomicAdd(a.ovf_next, 1ull);
         __syncthreads();

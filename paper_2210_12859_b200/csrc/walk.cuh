@@ -72,6 +72,8 @@ struct WalkArgs {
     uint32_t* wave_out;                    // ids still walking after this round
     unsigned long long* wave_n_out;
     int2* wave_state;                      // [m] (curr, prev) of suspended walks
+    int64_t resume_min;                    // >= this many over-budget queries: resume them with
+                                           // the plain grid instead of the CTA overflow pass
 };
 
 __device__ __forceinline__ uint64_t make_key(float d2, int32_t node) {
@@ -450,7 +452,10 @@ __global__ void __launch_bounds__(256, walk_min_blocks<KB>()) walk_kernel(const 
             }
         }
         w.finish(a);  // over budget: the partial list stays as the overflow pass's bound
-        if (over) a.ovf_ids[atomicAdd(a.ovf_count, 1ull)] = uint32_t(w.qi);
+        if (over) {
+            a.ovf_ids[atomicAdd(a.ovf_count, 1ull)] = uint32_t(w.qi);
+            a.wave_state[w.qi] = make_int2(w.curr, w.prev);  // for the resume pass
+        }
     }
     if (active) add_totals<STATS>(a, w.cnt.steps, w.cnt.visited, w.cnt.processed);
     else add_totals<STATS>(a, 0, 0, 0);
@@ -467,6 +472,7 @@ template <int D, int S, int KB, bool UNORDERED>
 __global__ void __launch_bounds__(256) walk_wave_kernel(const WalkArgs a) {
     const bool first = a.wave_in == nullptr;
     const int32_t items = first ? int32_t(a.m) : int32_t(*a.wave_n_in);
+    if (!first && a.resume_min > 0 && items < a.resume_min) return;  // few: the CTA pass takes them
     const int32_t stride = int32_t(gridDim.x * blockDim.x);  // a multiple of 32
     const unsigned lane = threadIdx.x & 31u;
     // whole warps iterate together so the survivor ballot can use a full mask

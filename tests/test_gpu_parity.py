@@ -196,11 +196,15 @@ def test_cpp_shim_against_reference():
     assert "OK" in out.stdout
 
 
-@pytest.mark.parametrize("budget", ["1", "3", "50"])
-def test_overflow_pass_is_exact(oracle, budget, monkeypatch):
+@pytest.mark.parametrize("budget,resume_min", [("1", "0"), ("3", "0"), ("50", "0"), ("2", "1"), ("40", "1")])
+def test_overflow_pass_is_exact(oracle, budget, resume_min, monkeypatch):
     """Queries stopped by the walk budget are finished by the CTA-per-query
-    overflow pass (overflow.cuh); results must stay bit-exact."""
+    overflow pass (overflow.cuh) or, when many overflow (FKD_RESUME_MIN=1
+    forces it), resumed from their parked (curr, prev) by the plain-grid resume
+    pass; results must stay bit-exact either way."""
     monkeypatch.setenv("FKD_BUDGET", budget)
+    if resume_min != "0":
+        monkeypatch.setenv("FKD_RESUME_MIN", resume_min)
     rng = oracle.instance_rng(777)
     for t in range(24):
         n = rng.next_int(1, 6000)
