@@ -44,6 +44,10 @@ WORKLOADS = {
            [("fcp", 1, float("inf"))]),
     "c2": ("kNN8 3D, N=1M uniform, M=1M queries, maxR=0.01", 1_000_000, 1_000_000, 3, "uniform",
            [("knn", 8, 0.01)]),
+    # C5 is strong scaling in the BASELINE (1B queries over 1/2/4/8 GPUs); run
+    # per rank as 1B / world queries with --workload c5
+    "c5": ("fcp 3D, N=100M uniform replicated tree, 1B uniform queries sharded over the GPUs",
+           100_000_000, 1_000_000_000, 3, "uniform", [("fcp", 1, float("inf"))]),
 }
 SEED = 1
 METRIC = "fcp & kNN(k=8) queries/sec, 3D float, N=10M, 1/2/4/8 B200 vs host CPU"
@@ -94,7 +98,7 @@ class ClockSampler:
         try:
             self.f = open(self.path, "w")
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
@@ -239,7 +243,15 @@ def run_b200(args) -> None:
     nodes_dev = replicate_tree(nodes_host, n, dim, dev) if world > 1 else nodes_dev
     tree = fk.KdTree.from_device(nodes_dev)
 
-    qs_host = gen_points(fk, gkind, query_stream(rank), m, dim)
+    strong = args.workload == "c5"
+    if strong:  # 1B queries split across the ranks (contiguous blocks of one stream)
+        from paper_2210_12859_b200.shard import shard_range
+
+        lo, hi = shard_range(m, world, rank)
+        m = hi - lo
+        qs_host = gen_points(fk, gkind, 2, hi, dim)[lo:hi].copy() if world > 1 else gen_points(fk, gkind, 2, m, dim)
+    else:
+        qs_host = gen_points(fk, gkind, query_stream(rank), m, dim)
     qs_dev = torch.from_numpy(qs_host).to(dev)
     outs = {}
     for kind, k, _ in batches:
@@ -291,7 +303,8 @@ def run_b200(args) -> None:
     if dist is not None:
         dist.barrier()
     t_step = max_over_ranks(sum(step_ms), dev) / args.steps / 1e3  # seconds, max over ranks
-    value = world * len(batches) * m / t_step
+    m_total = WORKLOADS[args.workload][2] if strong else world * m
+    value = len(batches) * m_total / t_step
 
     # ---- e2e through the host-buffer C ABI (pinned buffers), same metric
     import ctypes as C
@@ -323,7 +336,7 @@ def run_b200(args) -> None:
         t0 = time.perf_counter()
         e2e_step()
         e2e_times.append(time.perf_counter() - t0)
-    e2e_value = world * len(batches) * m / (max_over_ranks(sum(e2e_times), dev) / args.steps)
+    e2e_value = len(batches) * m_total / (max_over_ranks(sum(e2e_times), dev) / args.steps)
     # results of the e2e path must equal the device path (same queries)
     e2e_parity = True
     for kind, k, _ in batches:
@@ -365,7 +378,7 @@ def run_b200(args) -> None:
     line = {
         "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": desc, "tree_n": n, "queries_per_gpu": m, "dim": dim,
                    "batches_per_step": [("fcp" if kk == "fcp" else f"knn{k2}") for kk, k2, _ in batches],
                    "max_radius": [rr for _, _, rr in batches], "parallelism": f"query-sharded x{world}",
@@ -375,7 +388,8 @@ def run_b200(args) -> None:
                 "d2h_bytes_per_step": d2h, "results_equal_device_path": bool(e2e_parity),
                 "path": "fkd_run_batch (C ABI, pinned host buffers, chunked H2D/walk/D2H)"},
         "gpu_launches": launches // args.steps,
-        "gpu_launches_note": "own kernels per timed step (Morton keys + walk per batch); CUB sort kernels excluded",
+        "gpu_launches_note": "own kernels per timed step (per batch: Morton keys, walk, resume pass, "
+                             "overflow pass); CUB sort kernels excluded",
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": f"walk {kind}{'' if kind == 'fcp' else k} (dominant)",
@@ -394,7 +408,7 @@ def run_b200(args) -> None:
 def main():
     ap = argparse.ArgumentParser(description=__doc__)
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c3")
