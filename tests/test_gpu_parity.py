@@ -321,3 +321,36 @@ def test_binary_files_round_trip_with_reference(oracle, reference, tmp_path):
         f.write(b"FKDT" + (1).to_bytes(4, "little") + (3).to_bytes(4, "little") + (5000).to_bytes(8, "little"))
     with pytest.raises(fk.DataError, match="payload size does not match header"):
         fk.read_points_file_device(p3)
+
+
+def test_multi_replica_sharding(oracle, monkeypatch):
+    """fkd_tree_create with a device list shards a host batch across the
+    replicas (capi.cu fkd_run_batch); two replicas on GPU 0 exercise the
+    per-device workspaces, streams and result placement on a 1-GPU box."""
+    monkeypatch.setenv("FKD_CHUNK", "3000")
+    pts = oracle.random_points(12, 40000, 3)
+    nodes = oracle.build_tree(pts)
+    qs = oracle.random_points(13, 25001, 3)
+    one = fk.KdTree.from_level_order(nodes, devices=[0])
+    two = fk.KdTree.from_level_order(nodes, devices=[0, 0])
+    three = fk.build_tree(pts, devices=[0, 0, 0])
+    for kind, k, r in ((fk.QueryKind.fcp, 1, INF), (fk.QueryKind.knn, 8, 0.05), (fk.QueryKind.knn, 100, INF)):
+        opt = fk.BatchOptions(kind=kind, k=k, max_radius=r, collect_stats=True)
+        a, b, c = fk.run_batch(one, qs, opt), fk.run_batch(two, qs, opt), fk.run_batch(three, qs, opt)
+        assert a.hits.tobytes() == b.hits.tobytes() == c.hits.tobytes()
+        assert np.array_equal(a.counts, b.counts) and np.array_equal(a.counts, c.counts)
+        assert a.stats == b.stats == c.stats
+    bad = qs.copy()
+    bad[20000, 2] = np.nan  # lands in the second replica's shard: global index reported
+    with pytest.raises(fk.DataError, match="non-finite coordinate in point 20000"):
+        fk.run_batch(two, bad)
+
+
+def test_k_larger_than_tree_and_huge_k(oracle):
+    nodes = oracle.build_tree(oracle.random_points(21, 37, 2))
+    qs = oracle.random_points(22, 500, 2)
+    tree = fk.KdTree.from_level_order(nodes)
+    for k in (37, 38, 64, 65, 200, 1000):
+        res = fk.run_batch(tree, qs, fk.BatchOptions(kind=fk.QueryKind.knn, k=k))
+        c, h, _, _ = oracle.run_batch(nodes, qs, "knn", k)
+        assert np.array_equal(res.counts, c) and res.hits.tobytes() == h.tobytes()
