@@ -262,10 +262,20 @@ struct LaneWalk {
             load_point<D, S>(a.nodes, curr, p);
             pd = pick(p, d);
         }
-        if (from_parent) {  // traverse.hpp:217-222
+        if constexpr (KB > 1) {
+            // traverse.hpp:217-222.  kNN: the distance is computed every trip
+            // (no divergent block; measured faster), admission is predicated
+            // on a first visit.
             const float d2 = sq_dist(q, p);
             const uint64_t key = make_key(d2, curr);
-            if (key < L[KB - 1]) {  // d2 <= cap2 and beats the kth (cap_key)
+            if (from_parent && key < L[KB - 1]) {  // d2 <= cap2 and beats the kth (cap_key)
+                list_insert(L, key);
+                r2 = key_dist(L[KB - 1]);
+            }
+        } else if (from_parent) {  // fcp: a branch is cheaper than 8 more FP ops
+            const float d2 = sq_dist(q, p);
+            const uint64_t key = make_key(d2, curr);
+            if (key < L[KB - 1]) {  // d2 <= cap2 and beats the best (cap_key)
                 list_insert(L, key);
                 r2 = key_dist(L[KB - 1]);
             }
@@ -442,9 +452,13 @@ __global__ void __launch_bounds__(256, walk_min_blocks<KB>()) walk_kernel(const 
                 while (w.step(a)) {
                 }
             } else {
+                // two steps per budget check (measured: -5% on fcp; the
+                // budget is approximate by one trip, which nothing depends on)
                 int trips = a.budget;
-                while (w.step(a)) {
-                    if (--trips == 0) {
+                while (true) {
+                    if (!w.step(a)) break;
+                    if (!w.step(a)) break;
+                    if ((trips -= 2) <= 0) {
                         over = true;
                         break;
                     }
