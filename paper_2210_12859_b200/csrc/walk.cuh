@@ -452,13 +452,16 @@ __global__ void __launch_bounds__(256, walk_min_blocks<KB>()) walk_kernel(const 
                 while (w.step(a)) {
                 }
             } else {
-                // two steps per budget check (measured: -5% on fcp; the
-                // budget is approximate by one trip, which nothing depends on)
+                // four steps per budget check (measured on fcp: 2 steps -5%,
+                // 4 steps another -2%; the budget is approximate by a few
+                // trips, which nothing depends on)
                 int trips = a.budget;
                 while (true) {
                     if (!w.step(a)) break;
                     if (!w.step(a)) break;
-                    if ((trips -= 2) <= 0) {
+                    if (!w.step(a)) break;
+                    if (!w.step(a)) break;
+                    if ((trips -= 4) <= 0) {
                         over = true;
                         break;
                     }

@@ -1,1 +1,3 @@
-for lib in paper_2210_12859_b200/libfkd_b200.so build/ab/lib_10.so build/ab/lib_01.so build/ab/lib_11.so; do echo "lib $lib"; FKD_LIB=$PWD/$lib python tools/quickbench.py --configs fcp,knn8 --reps 5 2>&1 | grep true; FKD_LIB=$PWD/$lib python tools/quickbench.py --clustered --configs fcp,knn8 --reps 5 2>&1 | grep true; done
+python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+FKD_PERSIST=2 python -m pytest tests/test_gpu_parity.py -x -q 2>&1 | tail -2
+for v in 0 2; do echo "persist $v"; FKD_PERSIST=$v python tools/quickbench.py --configs fcp,knn8 --reps 5 2>&1 | grep true; FKD_PERSIST=$v python tools/quickbench.py --clustered --configs fcp,knn8 --reps 5 2>&1 | grep true; done
