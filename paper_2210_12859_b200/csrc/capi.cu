@@ -44,7 +44,7 @@ struct Tuning {
     int persistent = 0;
     int chunk = 64;
     int refill = 8;
-    int budget = 2048;
+    int budget = -1;  // -1: per kind (measured on C3: fcp 1024, kNN 3072 loop trips)
     int wave = 0;
     std::vector<int> rounds{64, 64, 128, 256, 512, 1024};
     int64_t resume_min = 0;  // 0: SMs x 2048
@@ -319,7 +319,8 @@ fkd_status enqueue(const fkd_tree* t, Replica& r, Workspace* w, const float* d_q
         a.chunk = tu.chunk;
         a.refill = tu.refill;
         a.persistent = tu.persistent;
-        a.budget = (stats || walk_bucket_of(k) == 0 || t->dim > 8 || a.persistent) ? 0 : tu.budget;
+        const int budget = tu.budget >= 0 ? tu.budget : (k == 1 ? 1024 : 3072);
+        a.budget = (stats || walk_bucket_of(k) == 0 || t->dim > 8 || a.persistent) ? 0 : budget;
         if (a.budget > 0) {
             FKD_CUDA(grow(w->ovf, w->ovf_cap, cm));
             FKD_CUDA(grow(w->wave_state, w->wave_state_cap, cm));

@@ -51,7 +51,7 @@ def run(ref, name, n, m, dim, data, batches, cpu_sample, unordered=(False,), rep
         for uo in unordered:
             # the unordered walk is measured as itself (no step budget /
             # overflow pass, which would finish it with ordered subtree walks)
-            os.environ["FKD_BUDGET"] = "0" if uo else os.environ.get("FKD_BUDGET_ORDERED", "2048")
+            os.environ["FKD_BUDGET"] = "0" if uo else os.environ.get("FKD_BUDGET_ORDERED", "-1")
             mm = m if not uo else min(m, unordered_m)
             opt = fk.BatchOptions(kind=fk.QueryKind[kind], k=k, max_radius=r, unordered=uo)
             dqm, cm, hm = dq[:mm], counts[:mm], hits[: mm * stride]
