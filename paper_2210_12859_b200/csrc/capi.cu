@@ -59,7 +59,7 @@ Tuning tuning() {
         if (const char* e = std::getenv("FKD_PERSIST")) x.persistent = std::atoi(e) != 0;
         if (const char* e = std::getenv("FKD_WORK_CHUNK")) x.chunk = std::max(32, std::atoi(e));
         if (const char* e = std::getenv("FKD_REFILL")) x.refill = std::min(32, std::max(1, std::atoi(e)));
-        if (const char* e = std::getenv("FKD_BUDGET")) x.budget = std::max(0, std::atoi(e));
+        if (const char* e = std::getenv("FKD_BUDGET")) x.budget = std::atoi(e);  // <0: per kind, 0: off
         if (const char* e = std::getenv("FKD_WAVE")) x.wave = std::atoi(e) != 0;
         if (const char* e = std::getenv("FKD_RESUME_MIN")) x.resume_min = std::atoll(e);
         if (const char* e = std::getenv("FKD_ROUNDS")) {  // e.g. "64,64,128"
