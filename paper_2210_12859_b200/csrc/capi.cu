@@ -767,14 +767,33 @@ fkd_status fkd_run_batch(const fkd_tree* t, const float* queries, int64_t m, int
     const bool want_stats = o->collect_stats != 0;
     const int ndev = int(t->reps.size());
     const int64_t per_dev = (m + ndev - 1) / ndev;
-    // Chunking: about 8 chunks per device shard (so the first H2D and the
-    // last D2H, which cannot overlap anything, are short), 0.5M..4M queries
-    // each; three workspaces (streams) per device keep the H2D engine, the
-    // SMs and the D2H engine busy at once.  FKD_CHUNK overrides.
-    const int64_t kChunk = [&] {
-        if (const char* e = std::getenv("FKD_CHUNK")) return std::max<int64_t>(1024, std::atoll(e));
-        return std::min<int64_t>(int64_t(4) << 20, std::max<int64_t>(int64_t(512) << 10, (per_dev + 7) / 8));
-    }();
+    // Chunking: a graduated schedule per device shard — small first chunks
+    // (the first H2D + walk cannot overlap anything), full-size middle
+    // chunks, small last chunks (the last D2H cannot overlap anything) — and
+    // four workspaces (streams) per device so the H2D engine, the SMs and
+    // the D2H engine stay busy at once.  FKD_CHUNK fixes a uniform size.
+    const char* chunk_env = std::getenv("FKD_CHUNK");
+    const int64_t full_chunk = chunk_env
+        ? std::max<int64_t>(1024, std::atoll(chunk_env))
+        : std::min<int64_t>(int64_t(4) << 20, std::max<int64_t>(int64_t(256) << 10, (per_dev + 7) / 8));
+    auto schedule = [&](int64_t total) {
+        std::vector<int64_t> sizes;
+        if (chunk_env || total <= 2 * full_chunk) {
+            for (int64_t b = 0; b < total; b += full_chunk) sizes.push_back(std::min(full_chunk, total - b));
+            return sizes;
+        }
+        const int64_t ramp[2] = {full_chunk / 4, full_chunk / 2};
+        std::vector<int64_t> tail_sizes{ramp[1], ramp[0]};
+        int64_t left = total - (ramp[0] + ramp[1]) * 2;
+        sizes.push_back(ramp[0]);
+        sizes.push_back(ramp[1]);
+        while (left > 0) {
+            sizes.push_back(std::min(full_chunk, left));
+            left -= sizes.back();
+        }
+        sizes.insert(sizes.end(), tail_sizes.begin(), tail_sizes.end());
+        return sizes;
+    };
 
     struct Job {
         int rep;
@@ -787,16 +806,17 @@ fkd_status fkd_run_batch(const fkd_tree* t, const float* queries, int64_t m, int
     for (int di = 0; di < ndev && err == FKD_OK; ++di) {
         const int64_t lo = std::min<int64_t>(m, di * per_dev), hi = std::min<int64_t>(m, lo + per_dev);
         if (hi <= lo) continue;
-        const int64_t nchunks = (hi - lo + kChunk - 1) / kChunk;
-        const int nws = int(std::min<int64_t>(nchunks, 3));
+        const std::vector<int64_t> sizes = schedule(hi - lo);
+        const int nws = int(std::min<size_t>(sizes.size(), 4));
         for (int j = 0; j < nws && err == FKD_OK; ++j) {
             Workspace* w = nullptr;
             err = acquire_ws(*t->reps[di], &w);
             if (err == FKD_OK) wss[di].push_back(w);
         }
-        for (int64_t c = 0; c < nchunks && err == FKD_OK; ++c) {
-            const int64_t b = lo + c * kChunk;
-            jobs.push_back(Job{di, wss[di][c % wss[di].size()], b, std::min(kChunk, hi - b)});
+        int64_t b = lo;
+        for (size_t c = 0; c < sizes.size() && err == FKD_OK; ++c) {
+            jobs.push_back(Job{di, wss[di][c % wss[di].size()], b, sizes[c]});
+            b += sizes[c];
         }
     }
     if (err == FKD_OK) {
