@@ -41,9 +41,6 @@ fkd_status fail(fkd_status s, const std::string& msg) {
 constexpr int64_t kSortChunk = int64_t(1) << 30;  // u32 ids, int item counts in CUB
 
 struct Tuning {
-    int persistent = 0;
-    int chunk = 64;
-    int refill = 8;
     int budget = -1;  // -1: per kind (measured on C3: fcp 1024, kNN 3072 loop trips)
     int wave = 0;
     std::vector<int> rounds{64, 64, 128, 256, 512, 1024};
@@ -51,14 +48,12 @@ struct Tuning {
 };
 
 // Launch tuning, overridable per call for experiments and tests:
-// FKD_PERSIST=0|1, FKD_WORK_CHUNK=<positions per fetch>,
-// FKD_REFILL=<idle lanes>, FKD_BUDGET=<loop trips before the overflow pass>.
+// FKD_BUDGET=<loop trips before the overflow pass; <0 per kind, 0 off>,
+// FKD_RESUME_MIN=<overflow count that selects the resume pass>,
+// FKD_WAVE=1 + FKD_ROUNDS=<t1,t2,..> (wave rounds, off: measured slower).
 Tuning tuning() {
     return [] {
         Tuning x;
-        if (const char* e = std::getenv("FKD_PERSIST")) x.persistent = std::atoi(e) != 0;
-        if (const char* e = std::getenv("FKD_WORK_CHUNK")) x.chunk = std::max(32, std::atoi(e));
-        if (const char* e = std::getenv("FKD_REFILL")) x.refill = std::min(32, std::max(1, std::atoi(e)));
         if (const char* e = std::getenv("FKD_BUDGET")) x.budget = std::atoi(e);  // <0: per kind, 0: off
         if (const char* e = std::getenv("FKD_WAVE")) x.wave = std::atoi(e) != 0;
         if (const char* e = std::getenv("FKD_RESUME_MIN")) x.resume_min = std::atoll(e);
@@ -314,13 +309,9 @@ fkd_status enqueue(const fkd_tree* t, Replica& r, Workspace* w, const float* d_q
         a.per_query = d_per_query ? d_per_query + base : nullptr;
         a.bad = w->small;
         a.id_base = id_offset + base;
-        a.work = w->small + 4;
         const Tuning tu = tuning();
-        a.chunk = tu.chunk;
-        a.refill = tu.refill;
-        a.persistent = tu.persistent;
         const int budget = tu.budget >= 0 ? tu.budget : (k == 1 ? 1024 : 3072);
-        a.budget = (stats || walk_bucket_of(k) == 0 || t->dim > 8 || a.persistent) ? 0 : budget;
+        a.budget = (stats || walk_bucket_of(k) == 0 || t->dim > 8) ? 0 : budget;
         if (a.budget > 0) {
             FKD_CUDA(grow(w->ovf, w->ovf_cap, cm));
             FKD_CUDA(grow(w->wave_state, w->wave_state_cap, cm));
@@ -345,10 +336,9 @@ fkd_status enqueue(const fkd_tree* t, Replica& r, Workspace* w, const float* d_q
             a.order = w->ids + half;
         }
         if (ev_mid && base == 0) FKD_CUDA(cudaEventRecord(ev_mid, st));
-        if (a.persistent) FKD_CUDA(cudaMemsetAsync(a.work, 0, sizeof(unsigned long long), st));
         const bool unordered = (o->flags & FKD_FLAG_UNORDERED) != 0;
         int nl = 0;
-        const bool wave = tu.wave && a.budget > 0 && !a.persistent;
+        const bool wave = tu.wave && a.budget > 0;
         if (wave) {
             // wave rounds (walk.cuh walk_wave_kernel); survivors of the last
             // round feed the overflow pass through the same id list

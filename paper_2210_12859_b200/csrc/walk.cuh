@@ -57,10 +57,6 @@ struct WalkArgs {
     fkd_query_stats* per_query; // [m] or null (STATS)
     unsigned long long* bad;    // min id of a non-finite query
     int64_t id_base;            // added to query ids reported through `bad`
-    unsigned long long* work;   // persistent kernel: next unclaimed walk position
-    int32_t chunk;              // persistent kernel: positions claimed per fetch
-    int32_t refill;             // persistent kernel: idle lanes that trigger a refill
-    int32_t persistent;         // launch the persistent lane-refill kernel
     int32_t budget;             // loop trips before a query moves to the overflow pass (0 = none)
     uint32_t* ovf_ids;          // [m] ids of queries over budget
     unsigned long long* ovf_count;
@@ -529,68 +525,6 @@ __global__ void __launch_bounds__(256) walk_wave_kernel(const WalkArgs a) {
             if (park) a.wave_out[base + __popc(mask & ((1u << lane) - 1u))] = uint32_t(w.qi);
         }
     }
-}
-
-// Persistent warps with lane refill.  Each warp takes chunks of walk
-// positions from a global counter; whenever at least `refill` lanes have
-// finished their query, those lanes start the next positions of the chunk
-// (order is preserved within a warp's chunk, so Morton neighbours stay
-// together).  Removes both the warp-level trip-count imbalance (a warp no
-// longer waits for its slowest query) and the grid tail.
-template <int D, int S, int KB, bool STATS, bool UNORDERED>
-__global__ void __launch_bounds__(256) walk_persistent_kernel(const WalkArgs a) {
-    unsigned long long* __restrict__ work = a.work;
-    const int chunk = a.chunk, refill = a.refill;
-    const unsigned lane = threadIdx.x & 31u;
-    const unsigned lt = (1u << lane) - 1u;
-    LaneWalk<D, S, KB, STATS, UNORDERED> w;
-    bool active = false;
-    int64_t cursor = 0, end = 0;  // warp-uniform
-    bool exhausted = false;
-    unsigned long long ts = 0, tv = 0, tp = 0;
-    while (true) {
-        const unsigned idle = __ballot_sync(0xffffffffu, !active);
-        if (!exhausted && (idle == 0xffffffffu || __popc(idle) >= refill)) {
-            const int need = __popc(idle);
-            const int r = __popc(idle & lt);
-            const int64_t avail = end - cursor;
-            int64_t mine = (!active && r < avail) ? cursor + r : -1;
-            if (need > avail) {
-                unsigned long long base = 0;
-                if (lane == 0) base = atomicAdd(work, (unsigned long long)chunk);
-                base = __shfl_sync(0xffffffffu, base, 0);
-                if (int64_t(base) >= a.m) {
-                    exhausted = true;
-                    cursor = end;
-                } else {
-                    const int64_t nb = int64_t(base);
-                    const int64_t ne = nb + chunk < a.m ? nb + chunk : a.m;
-                    if (!active && r >= avail && nb + (r - avail) < ne) mine = nb + (r - avail);
-                    cursor = nb + (need - avail);
-                    end = ne;
-                    if (cursor > end) cursor = end;
-                }
-            } else {
-                cursor += need;
-            }
-            if (mine >= 0) active = w.init(a, mine);
-            if (active && a.n == 0) {
-                w.finish(a);
-                active = false;
-            }
-        }
-        if (exhausted && __all_sync(0xffffffffu, !active)) break;
-        if (active && !w.step(a)) {
-            w.finish(a);
-            if constexpr (STATS) {
-                ts += w.cnt.steps;
-                tv += w.cnt.visited;
-                tp += w.cnt.processed;
-            }
-            active = false;
-        }
-    }
-    add_totals<STATS>(a, ts, tv, tp);
 }
 
 // ---------------------------------------------------------------------------

@@ -36,17 +36,7 @@ void launch_overflow(const WalkArgs& a, cudaStream_t st) {
 
 template <int D, int S, int KB, bool STATS, bool UNORDERED>
 void launch_one(const WalkArgs& a, cudaStream_t st) {
-    if constexpr (KB >= 64) {  // 128 list registers: the persistent kernel would spill
-        walk_kernel<D, S, KB, STATS, UNORDERED><<<walk_blocks(a.m, 256), 256, 0, st>>>(a);
-    } else if (a.persistent) {
-        auto kern = walk_persistent_kernel<D, S, KB, STATS, UNORDERED>;
-        static const unsigned cap = persistent_blocks(kern, int64_t(1) << 40);
-        const int64_t need = (a.m + 255) / 256;
-        const unsigned grid = unsigned(need < cap ? need : cap);
-        kern<<<grid, 256, 0, st>>>(a);
-    } else {
-        walk_kernel<D, S, KB, STATS, UNORDERED><<<walk_blocks(a.m, 256), 256, 0, st>>>(a);
-    }
+    walk_kernel<D, S, KB, STATS, UNORDERED><<<walk_blocks(a.m, 256), 256, 0, st>>>(a);
 }
 
 template <int D, int S, int KB, bool UNORDERED>
