@@ -271,7 +271,8 @@ fkd_status enqueue(const fkd_tree* t, Replica& r, Workspace* w, const float* d_q
         return FKD_OK;
     }
     const bool sort = use_morton(t, o, m);
-    const int64_t chunk = sort ? std::min<int64_t>(m, kSortChunk) : m;
+    // sub-batches of <= 2^30 positions: u32 ids in the sort and int32 query ids in the walk
+    const int64_t chunk = std::min<int64_t>(m, kSortChunk);
     if (sort) {
         if (2 * chunk > w->key_cap) {
             cudaFree(w->keys);
