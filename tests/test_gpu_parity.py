@@ -354,3 +354,38 @@ def test_k_larger_than_tree_and_huge_k(oracle):
         res = fk.run_batch(tree, qs, fk.BatchOptions(kind=fk.QueryKind.knn, k=k))
         c, h, _, _ = oracle.run_batch(nodes, qs, "knn", k)
         assert np.array_equal(res.counts, c) and res.hits.tobytes() == h.tobytes()
+
+
+@pytest.mark.parametrize("shape", ["identical", "collinear", "two_values", "pow2"])
+def test_degenerate_trees(oracle, shape, monkeypatch):
+    """All-tie inputs: every distance equal (identical points) or planes that
+    never separate (collinear, two values).  Every subtree stays in range, so
+    walks are long (budget -> overflow / resume passes) and every answer is
+    decided by the node-index tie rule (traverse.hpp:80-83)."""
+    rng = np.random.default_rng(7)
+    if shape == "identical":
+        pts = np.full((3000, 3), 0.25, np.float32)
+    elif shape == "collinear":
+        t = rng.random(4000, dtype=np.float32)
+        pts = np.stack([t, np.full_like(t, 0.5), np.full_like(t, 0.5)], 1)
+    elif shape == "two_values":
+        pts = rng.integers(0, 2, size=(4000, 2)).astype(np.float32)
+    else:
+        pts = rng.random((4095, 4), dtype=np.float32)
+    nodes = oracle.build_tree(pts)
+    qs = np.concatenate([pts[:50], rng.random((250, pts.shape[1]), dtype=np.float32)])
+    tree = fk.KdTree.from_level_order(nodes)
+    for budget in ("-1", "5"):
+        monkeypatch.setenv("FKD_BUDGET", budget)
+        for k, r in ((0, INF), (8, INF), (64, 0.1), (100, INF)):
+            res = fk.run_batch(tree, qs, fk.BatchOptions(kind=_kind(k), k=max(k, 1), max_radius=r))
+            c, h, _, _ = oracle.run_batch(nodes, qs, "knn" if k else "fcp", max(k, 1), r)
+            assert np.array_equal(res.counts, c), (shape, budget, k)
+            assert res.hits.tobytes() == h.tobytes(), (shape, budget, k)
+    pts2 = rng.random((4096, 3), dtype=np.float32)  # exactly 2^12 nodes: one node on the last level
+    nodes2 = oracle.build_tree(pts2)
+    q3 = np.ascontiguousarray(qs[:, :3]) if qs.shape[1] >= 3 else rng.random((300, 3), dtype=np.float32)
+    res = fk.run_batch(fk.KdTree.from_level_order(nodes2), q3,
+                       fk.BatchOptions(kind=fk.QueryKind.knn, k=4, collect_stats=True))
+    c, h, st, _ = oracle.run_batch(nodes2, q3, "knn", 4)
+    assert res.hits.tobytes() == h.tobytes() and res.stats.nodes_processed == int(st["nodes_processed"])
