@@ -1,2 +1,2 @@
-FKD_QPL=4 python -m pytest tests/test_gpu_parity.py -x -q 2>&1 | tail -2
-for v in 1 2 4 8; do echo "qpl $v"; FKD_QPL=$v python tools/quickbench.py --configs fcp,knn8 --reps 3 2>&1 | grep true; FKD_QPL=$v python tools/quickbench.py --clustered --configs fcp,knn8 --reps 3 2>&1 | grep true; done
+for b in 512 768 1024; do echo "fcp budget $b"; FKD_BUDGET=$b python tools/quickbench.py --clustered --configs fcp --reps 5 2>&1 | grep true; done
+for b in 2048 3072; do echo "knn budget $b"; FKD_BUDGET=$b python tools/quickbench.py --clustered --configs knn8 --reps 5 2>&1 | grep true; done
