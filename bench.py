@@ -154,7 +154,10 @@ def run_reference(args) -> None:
     ref = Reference()
     threads = ref.hardware_threads()
     pts = gen_points(fk, gkind, 1, n, dim)
-    nodes = ref.build_tree(pts)  # flatkd::build_tree (untimed, as bench.cpp does)
+    # the tree is input, not the path: flatkd::build_tree (untimed, as bench.cpp
+    # does); above 20M points its single-threaded build takes minutes (155 s at
+    # 100M), so the byte-identical multi-threaded host builder stands in
+    nodes = ref.build_tree(pts) if n <= 20_000_000 else fk.build_level_order(pts)
     sample = min(m, args.ref_sample)
     qs = gen_points(fk, gkind, query_stream(0), m, dim)[:sample]
     times = []

@@ -1,2 +1,3 @@
-for b in 512 768 1024; do echo "fcp budget $b"; FKD_BUDGET=$b python tools/quickbench.py --clustered --configs fcp --reps 5 2>&1 | grep true; done
-for b in 2048 3072; do echo "knn budget $b"; FKD_BUDGET=$b python tools/quickbench.py --clustered --configs knn8 --reps 5 2>&1 | grep true; done
+python tools/e2e_diag.py 2>&1 | sed -n 2p
+FKD_OVF_CTAS=1 python tools/e2e_diag.py 2>&1 | sed -n 2p
+FKD_BUDGET=0 python tools/e2e_diag.py 2>&1 | sed -n 2p
