@@ -220,12 +220,19 @@ void release_ws(Replica& r, Workspace* w) {
 }
 
 int walk_bucket_of(int k) {
+    static const int reg_max = [] {  // experiment: route larger k to the heap kernel
+        const char* e = std::getenv("FKD_REG_MAXK");
+        return e ? std::atoi(e) : 64;
+    }();
+    if (k > reg_max) return 0;
     if (k <= 1) return 1;
     if (k <= 2) return 2;
     if (k <= 4) return 4;
     if (k <= 8) return 8;
     if (k <= 16) return 16;
+    if (k <= 20) return 20;
     if (k <= 32) return 32;
+    if (k <= 50) return 50;
     if (k <= 64) return 64;
     return 0;
 }

@@ -30,7 +30,7 @@ unsigned persistent_blocks(K kernel, int64_t m) {
 // persistent grid reads the device-side overflow count, so no host sync.
 template <int D, int S, int KB>
 void launch_overflow(const WalkArgs& a, cudaStream_t st) {
-    constexpr int T = KB >= 32 ? 256 : 512;
+    constexpr int T = KB >= 20 ? 256 : 512;
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -91,7 +91,9 @@ int launch_fixed(const WalkArgs& a, int KB, bool stats, bool unordered, int phas
         case 4: return launch_bucket<D, S, 4>(a, stats, unordered, phase, st);
         case 8: return launch_bucket<D, S, 8>(a, stats, unordered, phase, st);
         case 16: return launch_bucket<D, S, 16>(a, stats, unordered, phase, st);
+        case 20: return launch_bucket<D, S, 20>(a, stats, unordered, phase, st);
         case 32: return launch_bucket<D, S, 32>(a, stats, unordered, phase, st);
+        case 50: return launch_bucket<D, S, 50>(a, stats, unordered, phase, st);
         case 64: return launch_bucket<D, S, 64>(a, stats, unordered, phase, st);
         default: return 0;
     }

@@ -1,3 +1,2 @@
-python tools/e2e_diag.py 2>&1 | sed -n 2p
-FKD_OVF_CTAS=1 python tools/e2e_diag.py 2>&1 | sed -n 2p
-FKD_BUDGET=0 python tools/e2e_diag.py 2>&1 | sed -n 2p
+python tools/kbench.py
+FKD_REG_MAXK=16 python tools/kbench.py

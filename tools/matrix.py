@@ -103,6 +103,10 @@ def main():
                                    (8, 1_000_000, 20_000, 2_000)):
             run(ref, f"C4-{dim}D", 10_000_000, m, dim, "uniform", [("knn", 16, INF)], sample,
                 unordered=(False, True), reps=2, unordered_m=um)
+    if "paper" in only:  # PAPER.md Table 1 setting: 4-D uniform, N=10M, M=10M (RTX 3090 Ti numbers)
+        run(ref, "paper-4D", 10_000_000, 10_000_000, 4, "uniform",
+            [("fcp", 1, INF), ("knn", 4, INF), ("knn", 8, INF), ("knn", 20, INF), ("knn", 50, INF),
+             ("knn", 4, 0.01), ("knn", 8, 0.01), ("knn", 20, 0.01), ("knn", 50, 0.01)], 100_000, reps=2)
     if "c5" in only:
         t0 = time.time()
         run(ref, "C5", 100_000_000, args.c5_queries, 3, "uniform", [("fcp", 1, INF)], 2_000_000, reps=2)
