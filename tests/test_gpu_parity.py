@@ -389,3 +389,39 @@ def test_degenerate_trees(oracle, shape, monkeypatch):
                        fk.BatchOptions(kind=fk.QueryKind.knn, k=4, collect_stats=True))
     c, h, st, _ = oracle.run_batch(nodes2, q3, "knn", 4)
     assert res.hits.tobytes() == h.tobytes() and res.stats.nodes_processed == int(st["nodes_processed"])
+
+
+def test_concurrent_callers_share_one_tree(oracle):
+    """any number of concurrent callers may share a tree.  Host
+    threads (ctypes drops the GIL) run different batches at once through the
+    host path and the single-query entry points; each gets its own pooled
+    workspace and stream."""
+    import threading
+
+    nodes = oracle.build_tree(oracle.random_points(61, 50000, 3))
+    tree = fk.KdTree.from_level_order(nodes)
+    jobs = []
+    for t in range(8):
+        qs = oracle.random_points(100 + t, 20000 + 997 * t, 3)
+        k = (0, 1, 4, 8, 16, 20, 50, 100)[t]
+        jobs.append((qs, k, oracle.run_batch(nodes, qs, "knn" if k else "fcp", max(k, 1), 0.2)))
+    errors = []
+
+    def worker(i):
+        qs, k, (c, h, _, _) = jobs[i]
+        try:
+            for _ in range(3):
+                res = fk.run_batch(tree, qs, fk.BatchOptions(kind=_kind(k), k=max(k, 1), max_radius=0.2))
+                assert np.array_equal(res.counts, c) and res.hits.tobytes() == h.tobytes()
+                q0 = qs[i]
+                one = fk.knn(tree, q0, max(k, 1), 0.2) if k else fk.fcp(tree, q0, 0.2)
+                assert one is not None or k == 0
+        except Exception as e:  # noqa: BLE001
+            errors.append((i, repr(e)))
+
+    threads = [threading.Thread(target=worker, args=(i,)) for i in range(8)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    assert not errors, errors
