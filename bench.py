@@ -366,6 +366,7 @@ def run_b200(args) -> None:
     t_walk = float(np.mean(walk_ms[dom])) / 1e3
     achieved = m * bq / t_walk / 1e9
     traffic = ncu_traffic(args.workload)
+    issue = ncu_traffic(args.workload + "_issue")
     per_batch = {}
     for b, (kk, k2, r2) in enumerate(batches):
         name = kk if kk == "fcp" else f"knn{k2}"
@@ -398,9 +399,18 @@ def run_b200(args) -> None:
                      "kernel": f"walk {kind}{'' if kind == 'fcp' else k} (dominant)",
                      "peak_source": peak_src,
                      "algorithmic_bytes_per_query": bq},
+        "issue_roofline": None if not issue else {
+            "bound": "issue (warp instructions; the walk is ALU/issue-bound, see DESIGN.md §6)",
+            "achieved": issue["knn8_warp_insts_per_launch"] / t_walk,
+            "peak": 4 * torch.cuda.get_device_properties(dev).multi_processor_count * float(
+                (sampler.summary().get("sm_mhz") or 1965.0)) * 1e6,
+            "unit": "warp-instructions/s", "kernel": "walk knn8",
+            "source": "instruction count per launch from profiles/traffic.json (ncu), time live"},
         "per_batch": per_batch,
         "clocks": sampler.summary(),
     }
+    if line.get("issue_roofline"):
+        line["issue_roofline"]["frac"] = line["issue_roofline"]["achieved"] / line["issue_roofline"]["peak"]
     if cpu is not None:
         line["cpu_baseline"] = cpu
     print(json.dumps(line), flush=True)
