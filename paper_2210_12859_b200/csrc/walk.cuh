@@ -284,50 +284,57 @@ struct LaneWalk {
         else
             qd = pick(q, d);
         const float sd = __fsub_rn(qd, pd);                         // 226
-        const int cs = sd > 0.0f;                                  // 227
+        const bool cs = sd > 0.0f;                                 // 227
         const bool fir = __fmul_rn(sd, sd) <= r2;                  // 230
-        const int32_t parent = ((curr + 1) >> 1) - 1;              // 205
+        const int32_t parent = (curr - 1) >> 1;                    // 205: (c+1)/2-1, root -> -1
+        const int32_t l = 2 * curr + 1, r = l + 1;
         int32_t next;
+        bool down;
         if constexpr (!UNORDERED) {
-            const int32_t close = 2 * curr + 1 + cs;               // 228
-            const int32_t far = 2 * curr + 2 - cs;                 // 229
-            next = from_parent ? close : ((prev == close && fir) ? far : parent);
-            if (next >= n) {  // empty slot: bounce + return visit, in registers
-                cnt.step(2, 1, 0);
-                next = (next == close && fir) ? far : parent;
-                if (next >= n) {
-                    cnt.step(2, 1, 0);
-                    next = parent;
-                }
+            const int32_t close = cs ? r : l;                      // 228
+            const int32_t far = cs ? l : r;                        // 229
+            // 232-238 with the bounces off empty slots (206-212) folded in:
+            // from the parent, an empty close slot bounces straight back,
+            // which is a return from the close child; an empty far slot
+            // bounces back, which is a return from the far child (-> parent).
+            const bool close_ok = close < n;
+            const bool go_close = from_parent && close_ok;
+            const bool try_far = from_parent ? !close_ok : prev == close;
+            const bool far_ok = far < n;
+            const bool go_far = try_far && fir && far_ok;
+            if constexpr (STATS) {
+                if (from_parent && !close_ok) cnt.step(2, 1, 0);
+                if (try_far && fir && !far_ok) cnt.step(2, 1, 0);
             }
+            down = go_close || go_far;
+            next = go_close ? close : (go_far ? far : parent);
         } else {
             // left-first order; a child is entered iff it is on the query's
             // side or its plane is within the radius
-            const int32_t left = 2 * curr + 1, right = 2 * curr + 2;
             const bool enter_left = !cs || fir, enter_right = cs || fir;
             if (from_parent)
-                next = enter_left ? left : (enter_right ? right : parent);
+                next = enter_left ? l : (enter_right ? r : parent);
             else
-                next = (prev == left && enter_right) ? right : parent;
+                next = (prev == l && enter_right) ? r : parent;
             if (next >= n) {
                 cnt.step(2, 1, 0);
-                next = (next == left && enter_right) ? right : parent;
+                next = (next == l && enter_right) ? r : parent;
                 if (next >= n) {
                     cnt.step(2, 1, 0);
                     next = parent;
                 }
             }
+            down = next != parent;
         }
-        if (next < 0) return false;  // 240-244
+        if (!down && curr == 0) return false;  // 240-244: the root stepped to -1
         if constexpr (kRot) {
-            const bool up = next == parent;
             float t[D];
 #pragma unroll
-            for (int j = 0; j < D; ++j) t[j] = up ? qr[(j + D - 1) % D] : qr[(j + 1) % D];
+            for (int j = 0; j < D; ++j) t[j] = down ? qr[(j + 1) % D] : qr[(j + D - 1) % D];
 #pragma unroll
             for (int j = 0; j < D; ++j) qr[j] = t[j];
         } else {
-            d = next == parent ? dim_down<D>(d) : dim_up<D>(d);
+            d = down ? dim_up<D>(d) : dim_down<D>(d);
         }
         prev = curr;
         curr = next;

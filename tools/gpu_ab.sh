@@ -1,1 +1,2 @@
-for b in 8 5; do echo "bits $b"; FKD_MORTON_BITS=$b python tools/quickbench.py --configs fcp,knn8 --reps 5 2>&1 | grep true; FKD_MORTON_BITS=$b python tools/quickbench.py --clustered --configs fcp,knn8 --reps 5 2>&1 | grep true; done
+python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+for i in 1 2; do python tools/quickbench.py --configs fcp,knn8 --reps 5 2>&1 | grep true; python tools/quickbench.py --clustered --configs fcp,knn8 --reps 5 2>&1 | grep true; done
