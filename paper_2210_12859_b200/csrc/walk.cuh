@@ -154,11 +154,14 @@ __device__ __forceinline__ void load_point(const float* __restrict__ nodes, int3
 
 template <int KB>
 __device__ __forceinline__ void list_insert(uint64_t (&L)[KB], uint64_t x) {
+    // one 64-bit compare per slot feeds both selects (the compiler otherwise
+    // evaluates L < x and x < L separately: 4 ISETP instead of 2)
 #pragma unroll
     for (int j = 0; j < KB; ++j) {
-        const uint64_t lo = L[j] < x ? L[j] : x;
-        x = L[j] < x ? x : L[j];
-        L[j] = lo;
+        const uint64_t Lj = L[j];
+        const bool keep = Lj < x;
+        L[j] = keep ? Lj : x;
+        x = keep ? x : Lj;
     }
 }
 
