@@ -507,6 +507,33 @@ static fkd_status make_replica(fkd_tree* t, int dev, const float* src, bool src_
     return FKD_OK;
 }
 
+// Further replicas are copied device to device from the first one (over
+// NVLink / NVSwitch between B200s; cudaMemcpyPeer stages through the host
+// only when peer access is unavailable) — SURVEY §8(e): one upload, then a
+// fan-out of the packed store.
+static fkd_status peer_replica(fkd_tree* t, int dev) {
+    Replica* src = t->reps.front();
+    auto* r = new Replica();
+    r->device = dev;
+    t->reps.push_back(r);
+    if (t->n == 0) return FKD_OK;
+    const size_t bytes = size_t(t->n) * t->stride * sizeof(float);
+    DeviceGuard g(dev);
+    FKD_CUDA(cudaMalloc(&r->nodes, bytes));
+    if (dev == src->device) {
+        FKD_CUDA(cudaMemcpy(r->nodes, src->nodes, bytes, cudaMemcpyDeviceToDevice));
+    } else {
+        int can = 0;
+        cudaDeviceCanAccessPeer(&can, dev, src->device);
+        if (can) {
+            cudaError_t e = cudaDeviceEnablePeerAccess(src->device, 0);
+            if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+        }
+        FKD_CUDA(cudaMemcpyPeer(r->nodes, dev, src->nodes, src->device, bytes));
+    }
+    return FKD_OK;
+}
+
 fkd_status fkd_tree_create(const float* level_order, int64_t n, int32_t dim,
                            const int32_t* devices, int32_t ndev, fkd_tree** out) {
     if (!out) return fail(FKD_INVALID_ARGUMENT, "null output");
@@ -541,12 +568,13 @@ fkd_status fkd_tree_create(const float* level_order, int64_t n, int32_t dim,
         cudaGetDevice(&cur);
         devs.push_back(cur);
     }
-    for (int dev : devs) {
+    for (size_t i = 0; i < devs.size(); ++i) {
+        const int dev = devs[i];
         if (dev < 0 || dev >= count) {
             fkd_tree_destroy(t);
             return fail(FKD_INVALID_ARGUMENT, "device id out of range");
         }
-        fkd_status s = make_replica(t, dev, level_order, false, nullptr);
+        fkd_status s = i == 0 ? make_replica(t, dev, level_order, false, nullptr) : peer_replica(t, dev);
         if (s != FKD_OK) {
             fkd_tree_destroy(t);
             return s;

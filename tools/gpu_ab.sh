@@ -1,2 +1,2 @@
-python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-for i in 1 2; do python tools/quickbench.py --configs fcp,knn8 --reps 5 2>&1 | grep true; python tools/quickbench.py --clustered --configs fcp,knn8 --reps 5 2>&1 | grep true; done
+for b in 768 1024 1536; do echo "fcp budget $b"; FKD_BUDGET=$b python tools/quickbench.py --clustered --configs fcp --reps 5 2>&1 | grep true; done
+for b in 2048 3072 4096; do echo "knn budget $b"; FKD_BUDGET=$b python tools/quickbench.py --clustered --configs knn8 --reps 5 2>&1 | grep true; done
