@@ -1,1 +1,2 @@
-for lib in paper_2210_12859_b200/libfkd_b200.so build/ab/lib_mb6.so build/ab/lib_mb8.so; do echo "lib $lib"; FKD_LIB=$PWD/$lib python tools/quickbench.py --configs knn8 --reps 5 2>&1 | grep true; FKD_LIB=$PWD/$lib python tools/quickbench.py --clustered --configs knn8 --reps 5 2>&1 | grep true; done
+python -m pytest tests -m gpu -x -q 2>&1 | tail -1
+for v in 0 1; do echo "align $v"; FKD_SIBLING_ALIGN=$v python tools/quickbench.py --configs fcp,knn8 --reps 5 2>&1 | grep true; FKD_SIBLING_ALIGN=$v python tools/quickbench.py --clustered --configs fcp,knn8 --reps 5 2>&1 | grep true; done
