@@ -17,6 +17,8 @@
 #include <array>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
+#include <ostream>
 #include <limits>
 #include <memory>
 #include <optional>
@@ -81,6 +83,26 @@ struct QueryStats {
     static constexpr int state_node_ids = 2;
 };
 static_assert(sizeof(QueryStats) == sizeof(fkd_query_stats));
+
+// traverse.hpp:56-68
+struct TraceEvent {
+    enum class Kind : std::uint8_t { processed, bounced };
+    Kind kind = Kind::processed;
+    std::int32_t node = -1;
+    bool operator==(const TraceEvent&) const = default;
+};
+using Trace = std::vector<TraceEvent>;
+
+inline std::string trace_to_text(const Trace& trace) {  // traverse.cpp:7-16
+    std::string out;
+    for (const TraceEvent& e : trace) {
+        out += e.kind == TraceEvent::Kind::processed ? 'P' : 'B';
+        out += ' ';
+        out += std::to_string(e.node);
+        out += '\n';
+    }
+    return out;
+}
 
 enum class Engine { stack_free, recursive };  // batch.hpp:10
 enum class QueryKind { fcp, knn };            // batch.hpp:11
@@ -220,9 +242,48 @@ inline BatchResult run_batch(const KdTree& tree, const PointSet& queries, const 
     return run_batch(tree, queries.raw().data(), queries.size(), queries.dim(), options);
 }
 
-// traverse.cpp:25-39 over runtime-dimension spans
+namespace detail {
+
+// A traced single query: the GPU walks it with the literal state machine
+// (fkd_trace_batch) and returns the reference's event list.
+inline std::vector<Hit> traced(const KdTree& tree, std::span<const float> query, int kind, int k,
+                               float max_radius, QueryStats* stats, Trace* trace) {
+    const int stride = kind == FKD_KNN ? k : 1;
+    std::vector<Hit> out(static_cast<std::size_t>(stride > 0 ? stride : 1));
+    int32_t count = 0;
+    fkd_query_stats st{0, 0, 0};
+    int64_t cap = 1 << 16, len = 0;
+    std::vector<int32_t> ev;
+    for (;;) {  // grow the buffer until the whole trace fits
+        ev.assign(static_cast<std::size_t>(cap), 0);
+        check(fkd_trace_batch(tree.handle(), query.data(), 1, static_cast<int32_t>(query.size()), kind, k,
+                              max_radius, &count, reinterpret_cast<fkd_hit*>(out.data()), &st, ev.data(), cap,
+                              &len));
+        if (len <= cap) break;
+        cap = len;
+    }
+    if (stats) *stats = QueryStats{st.steps, st.nodes_visited, st.nodes_processed};
+    trace->clear();
+    for (int64_t i = 0; i < len; ++i) {
+        const int32_t e = ev[static_cast<std::size_t>(i)];
+        trace->push_back(e >= 0 ? TraceEvent{TraceEvent::Kind::processed, e}
+                                : TraceEvent{TraceEvent::Kind::bounced, ~e});
+    }
+    out.resize(static_cast<std::size_t>(count));
+    return out;
+}
+
+}  // namespace detail
+
+// traverse.cpp:25-39 over runtime-dimension spans (same argument list,
+// including the optional stats and trace outputs, traverse.hpp:297-306)
 inline std::optional<Hit> fcp(const KdTree& tree, std::span<const float> query,
-                              float max_radius = kInfRadius, QueryStats* stats = nullptr) {
+                              float max_radius = kInfRadius, QueryStats* stats = nullptr,
+                              Trace* trace = nullptr) {
+    if (trace) {
+        auto h = detail::traced(tree, query, FKD_FCP, 1, max_radius, stats, trace);
+        return h.empty() ? std::nullopt : std::optional<Hit>(h[0]);
+    }
     Hit h;
     int32_t count = 0;
     fkd_query_stats st{0, 0, 0};
@@ -233,7 +294,9 @@ inline std::optional<Hit> fcp(const KdTree& tree, std::span<const float> query,
 }
 
 inline std::vector<Hit> knn(const KdTree& tree, std::span<const float> query, int k,
-                            float max_radius = kInfRadius, QueryStats* stats = nullptr) {
+                            float max_radius = kInfRadius, QueryStats* stats = nullptr,
+                            Trace* trace = nullptr) {
+    if (trace && k >= 1) return detail::traced(tree, query, FKD_KNN, k, max_radius, stats, trace);
     std::vector<Hit> out(static_cast<std::size_t>(k > 0 ? k : 1));
     int32_t count = 0;
     fkd_query_stats st{0, 0, 0};
@@ -242,6 +305,33 @@ inline std::vector<Hit> knn(const KdTree& tree, std::span<const float> query, in
     if (stats) *stats = QueryStats{st.steps, st.nodes_visited, st.nodes_processed};
     out.resize(static_cast<std::size_t>(count));
     return out;
+}
+
+// batch.cpp:136-158 (io::format_float is "%.9g", io.cpp:163-167)
+inline void write_query_results(std::ostream& out, const BatchResult& result) {
+    auto fmt = [](float v) {
+        char buf[48];
+        std::snprintf(buf, sizeof(buf), "%.9g", static_cast<double>(v));
+        return std::string(buf);
+    };
+    std::string line;
+    for (std::size_t q = 0; q < result.counts.size(); ++q) {
+        line.clear();
+        const auto hits = result.hits_for(static_cast<int>(q));
+        if (result.stride == 1) {
+            line = hits.empty() ? std::string("-1,inf") : std::to_string(hits[0].node) + ',' + fmt(hits[0].distance());
+        } else {
+            line = std::to_string(hits.size());
+            for (const Hit& h : hits) {
+                line += ',';
+                line += std::to_string(h.node);
+                line += ',';
+                line += fmt(h.distance());
+            }
+        }
+        line += '\n';
+        out << line;
+    }
 }
 
 // ---- templated float point types (north_star: "fcp and kNN entry points

@@ -3,6 +3,7 @@
 // and flatkd::b200::run_batch (this library, GPU); results must be identical
 // byte for byte.  Needs a GPU; run by tests/test_gpu_parity.py.
 #include <cstdio>
+#include <sstream>
 #include <cstring>
 #include <stdexcept>
 #include <vector>
@@ -105,6 +106,45 @@ int main() {
             expect(same(ref, gpu), "tie-heavy results differ");
             expect(ref.stats.nodes_processed == gpu.stats.nodes_processed, "tie-heavy stats differ");
         }
+    }
+
+    // the standalone shim: its own types, traces and text output vs the reference
+    {
+        flatkd::b200::PointSet pts(3, data.raw());
+        const auto st_tree = flatkd::b200::build_tree(pts);
+        for (int i = 0; i < 50; ++i) {
+            const auto q = queries[i];
+            flatkd::QueryStats rs;
+            flatkd::Trace rt;
+            const auto rk = flatkd::knn(cpu_tree, q, 4, 0.1f, &rs, &rt);
+            flatkd::b200::QueryStats gs;
+            flatkd::b200::Trace gt;
+            const auto gk = flatkd::b200::knn(st_tree, q, 4, 0.1f, &gs, &gt);
+            bool eq = rk.size() == gk.size() && rt.size() == gt.size() && rs.steps == gs.steps &&
+                      rs.nodes_processed == gs.nodes_processed;
+            for (std::size_t j = 0; eq && j < rt.size(); ++j)
+                eq = rt[j].node == gt[j].node && int(rt[j].kind) == int(gt[j].kind);
+            expect(eq, "traced knn differs");
+            flatkd::Trace ft;
+            flatkd::b200::Trace fg;
+            flatkd::fcp(cpu_tree, q, flatkd::kInfRadius, nullptr, &ft);
+            flatkd::b200::fcp(st_tree, q, flatkd::b200::kInfRadius, nullptr, &fg);
+            expect(flatkd::trace_to_text(ft) == flatkd::b200::trace_to_text(fg), "fcp trace text differs");
+        }
+        flatkd::BatchOptions o;
+        o.kind = flatkd::QueryKind::knn;
+        o.k = 3;
+        o.max_radius = 0.05f;
+        const auto ref = flatkd::run_batch(cpu_tree, queries, o);
+        flatkd::b200::BatchOptions bo;
+        bo.kind = flatkd::b200::QueryKind::knn;
+        bo.k = 3;
+        bo.max_radius = 0.05f;
+        const auto gpu = flatkd::b200::run_batch(st_tree, flatkd::b200::PointSet(3, queries.raw()), bo);
+        std::ostringstream a, b;
+        flatkd::write_query_results(a, ref);
+        flatkd::b200::write_query_results(b, gpu);
+        expect(a.str() == b.str(), "write_query_results text differs");
     }
 
     // error mapping: the reference's exception types
