@@ -1,2 +1,1 @@
-python -m pytest tests -m gpu -x -q 2>&1 | tail -1
-for v in 0 1; do echo "align $v"; FKD_SIBLING_ALIGN=$v python tools/quickbench.py --configs fcp,knn8 --reps 5 2>&1 | grep true; FKD_SIBLING_ALIGN=$v python tools/quickbench.py --clustered --configs fcp,knn8 --reps 5 2>&1 | grep true; done
+for cfg in "8 4" "8 6" "12 4" "12 6" "16 6" "16 8"; do set -- $cfg; echo "div $1 streams $2"; FKD_CHUNK_DIV=$1 FKD_STREAMS=$2 python tools/e2e_diag.py 2>&1 | sed -n 2p; done
