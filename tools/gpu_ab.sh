@@ -1,1 +1,1 @@
-for cfg in "8 4" "8 6" "12 4" "12 6" "16 6" "16 8"; do set -- $cfg; echo "div $1 streams $2"; FKD_CHUNK_DIV=$1 FKD_STREAMS=$2 python tools/e2e_diag.py 2>&1 | sed -n 2p; done
+for lib in build/ab/lib_bub.so paper_2210_12859_b200/libfkd_b200.so build/ab/lib_s8.so; do echo "lib $lib"; FKD_LIB=$PWD/$lib python tools/kbench2.py; done
