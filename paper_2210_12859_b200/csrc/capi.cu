@@ -538,7 +538,8 @@ fkd_status fkd_tree_create(const float* level_order, int64_t n, int32_t dim,
                            const int32_t* devices, int32_t ndev, fkd_tree** out) {
     if (!out) return fail(FKD_INVALID_ARGUMENT, "null output");
     *out = nullptr;
-    if (n < 0 || n > int64_t(0x7fffffff)) return fail(FKD_DATA_ERROR, "tree size out of range");
+    // child slots 2c+1 / 2c+2 are int32 (traverse.hpp:228-229): fine below 2^30 nodes
+    if (n < 0 || n >= (int64_t(1) << 30)) return fail(FKD_DATA_ERROR, "tree size out of range (must be < 2^30)");
     if (dim < 0 || (n > 0 && dim < 1)) return fail(FKD_DATA_ERROR, "point set: negative dimension");
     if (n > 0 && !level_order) return fail(FKD_INVALID_ARGUMENT, "null tree data");
     int count = 0;
@@ -588,7 +589,8 @@ fkd_status fkd_tree_create_device(const float* d_level_order, int64_t n, int32_t
                                   fkd_tree** out) {
     if (!out) return fail(FKD_INVALID_ARGUMENT, "null output");
     *out = nullptr;
-    if (n < 0 || n > int64_t(0x7fffffff)) return fail(FKD_DATA_ERROR, "tree size out of range");
+    // child slots 2c+1 / 2c+2 are int32 (traverse.hpp:228-229): fine below 2^30 nodes
+    if (n < 0 || n >= (int64_t(1) << 30)) return fail(FKD_DATA_ERROR, "tree size out of range (must be < 2^30)");
     if (dim < 0 || (n > 0 && dim < 1)) return fail(FKD_DATA_ERROR, "point set: negative dimension");
     int count = 0;
     if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
