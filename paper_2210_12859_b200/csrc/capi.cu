@@ -93,6 +93,9 @@ struct Workspace {
     int device = 0;
     cudaStream_t stream = nullptr;  // own stream (host path)
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    // host path: this slot's last H2D / walk / D2H completion (timing disabled)
+    cudaEvent_t pe[3] = {nullptr, nullptr, nullptr};
+    cudaStream_t cin = nullptr, cout = nullptr;  // copy streams (first slot of a call)
     uint32_t* keys = nullptr;       // [2 * cap] keys in/out
     uint32_t* ids = nullptr;        // [2 * cap] ids in/out
     int64_t key_cap = 0;
@@ -129,6 +132,10 @@ struct Workspace {
         cudaFree(hits);
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
+        for (auto& e : pe)
+            if (e) cudaEventDestroy(e);
+        if (cin) cudaStreamDestroy(cin);
+        if (cout) cudaStreamDestroy(cout);
         if (stream) cudaStreamDestroy(stream);
     }
 };
@@ -204,6 +211,10 @@ fkd_status acquire_ws(Replica& r, Workspace** out) {
     cudaError_t e = cudaStreamCreateWithFlags(&w->stream, cudaStreamNonBlocking);
     for (auto& ev : w->ev)
         if (e == cudaSuccess) e = cudaEventCreate(&ev);
+    for (auto& ev : w->pe)
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&w->cin, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&w->cout, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaMalloc(&w->small, 16 * sizeof(unsigned long long));
     if (e == cudaSuccess) e = cudaMallocHost(&w->h_small, 16 * sizeof(unsigned long long));
     if (e != cudaSuccess) {
@@ -290,7 +301,7 @@ fkd_status enqueue(const fkd_tree* t, Replica& r, Workspace* w, const float* d_q
             FKD_CUDA(cudaMalloc(&w->ids, size_t(2 * chunk) * sizeof(uint32_t)));
             w->key_cap = 2 * chunk;
         }
-        const size_t need = morton_temp_bytes(chunk);
+        const size_t need = morton_temp_bytes(chunk, t->dim);
         if (need > w->sort_tmp_bytes) {
             cudaFree(w->sort_tmp);
             w->sort_tmp = nullptr;
@@ -798,7 +809,7 @@ fkd_status fkd_run_batch(const fkd_tree* t, const float* queries, int64_t m, int
     // Chunking: a graduated schedule per device shard — small first chunks
     // (the first H2D + walk cannot overlap anything), full-size middle
     // chunks (shard/8), small last chunks (the last D2H cannot overlap
-    // anything) — and six workspaces (streams) per device so the H2D engine,
+    // anything) — and four slots (workspaces) per device so the H2D engine,
     // the SMs and the D2H engine stay busy at once.  FKD_CHUNK fixes a
     // uniform size; FKD_CHUNK_DIV / FKD_STREAMS are experiment knobs.
     const char* chunk_env = std::getenv("FKD_CHUNK");
@@ -806,9 +817,9 @@ fkd_status fkd_run_batch(const fkd_tree* t, const float* queries, int64_t m, int
         const char* e = std::getenv("FKD_CHUNK_DIV");
         return e ? std::max(1, std::atoi(e)) : 8;
     }();
-    const int n_streams = [] {  // measured: 6 beats 4 by ~2.5% on C3 e2e
+    const int n_streams = [] {  // measured (decoupled copy streams): 4 slots beat 6 by ~5% on C3 kNN8 e2e
         const char* e = std::getenv("FKD_STREAMS");
-        return e ? std::max(1, std::atoi(e)) : 6;
+        return e ? std::max(1, std::atoi(e)) : 4;
     }();
     const int64_t full_chunk = chunk_env
         ? std::max<int64_t>(1024, std::atoll(chunk_env))
@@ -872,10 +883,19 @@ fkd_status fkd_run_batch(const fkd_tree* t, const float* queries, int64_t m, int
             }
         }
     }
-    // Enqueue: H2D -> order + walk -> D2H, per chunk; bad ids (offset by the
-    // chunk base) and stat totals accumulate on the device per workspace and
-    // are read once at the end.  A workspace's stream serialises its own
-    // chunks, so buffer reuse is safe; nothing here blocks the host until the
+    // Enqueue, per chunk c on slot s = c mod R (a slot = one workspace: its
+    // staging buffers and its compute stream):
+    //   copy-in stream : wait walk(c-R) [slot's q is free] ; H2D ; record in(s)
+    //   slot stream    : wait in(s), wait out(c-R) [slot's results are free] ;
+    //                    order + walk ; record walk(s)
+    //   copy-out stream: wait walk(s) ; D2H counts + hits ; record out(s)
+    // One H2D and one D2H stream per device keep both copy engines streaming
+    // in chunk order without queueing an H2D behind an unrelated D2H (which
+    // a per-slot H2D -> walk -> D2H stream would), and the walks of
+    // neighbouring chunks overlap each other's tails on the slot streams.
+    // Every wait names an event recorded earlier in host order.  Bad ids
+    // (offset by the chunk base) and stat totals accumulate on the device per
+    // slot and are read once at the end; nothing blocks the host until the
     // final synchronisation (with pinned caller buffers).
     for (int di = 0; di < ndev && err == FKD_OK; ++di) {
         DeviceGuard g(t->reps[di]->device);
@@ -889,17 +909,27 @@ fkd_status fkd_run_batch(const fkd_tree* t, const float* queries, int64_t m, int
         Replica& r = *t->reps[j.rep];
         DeviceGuard g(r.device);
         Workspace* w = j.w;
+        Workspace* io = wss[j.rep][0];
+        const bool reused = std::count_if(jobs.begin(), jobs.begin() + ji,
+                                          [&](const Job& x) { return x.w == w; }) > 0;
         int launches = 0, wl = 0;
         auto step = [&]() -> fkd_status {
+            if (reused) FKD_CUDA(cudaStreamWaitEvent(io->cin, w->pe[1], 0));
             FKD_CUDA(cudaMemcpyAsync(w->q, queries + j.base * dim, size_t(j.count) * dim * sizeof(float),
-                                     cudaMemcpyHostToDevice, w->stream));
+                                     cudaMemcpyHostToDevice, io->cin));
+            FKD_CUDA(cudaEventRecord(w->pe[0], io->cin));
+            FKD_CUDA(cudaStreamWaitEvent(w->stream, w->pe[0], 0));
+            if (reused) FKD_CUDA(cudaStreamWaitEvent(w->stream, w->pe[2], 0));
             fkd_status e = enqueue(t, r, w, w->q, j.count, o, cap2, w->counts, w->hits, nullptr,
                                    want_stats, w->stream, &launches, &wl, nullptr, nullptr, j.base);
             if (e != FKD_OK) return e;
+            FKD_CUDA(cudaEventRecord(w->pe[1], w->stream));
+            FKD_CUDA(cudaStreamWaitEvent(io->cout, w->pe[1], 0));
             FKD_CUDA(cudaMemcpyAsync(counts + j.base, w->counts, size_t(j.count) * sizeof(int32_t),
-                                     cudaMemcpyDeviceToHost, w->stream));
+                                     cudaMemcpyDeviceToHost, io->cout));
             FKD_CUDA(cudaMemcpyAsync(hits + j.base * k, w->hits, size_t(j.count) * k * sizeof(fkd_hit),
-                                     cudaMemcpyDeviceToHost, w->stream));
+                                     cudaMemcpyDeviceToHost, io->cout));
+            FKD_CUDA(cudaEventRecord(w->pe[2], io->cout));
             return FKD_OK;
         };
         err = step();
@@ -916,6 +946,13 @@ fkd_status fkd_run_batch(const fkd_tree* t, const float* queries, int64_t m, int
     unsigned long long bad = kNoBad, tot[3] = {0, 0, 0};
     for (int di = 0; di < ndev; ++di) {
         DeviceGuard g(t->reps[di]->device);
+        if (!wss[di].empty()) {
+            for (cudaStream_t cs : {wss[di][0]->cin, wss[di][0]->cout}) {
+                cudaError_t e = cudaStreamSynchronize(cs);
+                if (e != cudaSuccess && err == FKD_OK)
+                    err = fail(FKD_CUDA_ERROR, std::string("stream: ") + cudaGetErrorString(e));
+            }
+        }
         for (Workspace* w : wss[di]) {
             cudaError_t e = cudaStreamSynchronize(w->stream);
             if (e != cudaSuccess && err == FKD_OK)

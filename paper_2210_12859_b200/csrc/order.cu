@@ -3,13 +3,24 @@
 //
 // Keys: each coordinate is quantised to b bits over the TREE's bounding box
 // (computed once at tree creation, so no per-batch reduction pass), clamped,
-// and the D*b bits interleaved into a 32-bit key.  A CUB onesweep radix sort
-// of (key, query id) over exactly D*b bits yields order[]: walk position ->
-// query id.  The walk kernel gathers queries through order[] and scatters
+// and the D*b <= 24 bits interleaved into a key.  order[] (walk position ->
+// query id) groups equal keys in key order, built one of two ways:
+//   * counting sort (large batches): one pass computes the key and takes a
+//     rank inside its bin with an atomic, an exclusive scan over the 2^(D*b)
+//     bins gives bin offsets, one pass scatters id -> offset + rank.  Two
+//     reads of the batch instead of the onesweep's three digit passes; the
+//     order inside a bin is arbitrary (C3's fullest 24-bit bin holds 140 of
+//     10M queries, so the atomics barely contend);
+//   * CUB onesweep radix sort of (key, id) over D*b bits (small batches,
+//     where scanning 2^24 bins would dominate).  The walk kernel gathers queries through order[] and scatters
 // results to their own slots, so no permute / un-permute passes exist.
 // Ordering never changes results (every query is independent); it only makes
 // the 32 lanes of a warp walk neighbouring paths.
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include <algorithm>
+#include <cstdlib>
 
 #include <cstdint>
 #include <cstring>
@@ -27,11 +38,7 @@ int morton_bits_per_dim(int dim) {
 }
 
 template <int D>
-__global__ void __launch_bounds__(256)
-    morton_keys_kernel(const float* __restrict__ q, int64_t m, MortonFrame f,
-                       uint32_t* __restrict__ keys, uint32_t* __restrict__ ids) {
-    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= m) return;
+__device__ __forceinline__ uint32_t morton_key(const float* __restrict__ q, int64_t i, const MortonFrame& f) {
     const int b = f.bits;
     const float top = float((1u << b) - 1u);
     uint32_t c[D];
@@ -46,14 +53,67 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
         for (int d = 0; d < D; ++d) key = (key << 1) | ((c[d] >> bit) & 1u);
     }
+    return key;
+}
+
+// counting sort, pass 1: key + rank inside the key's bin
+template <int D>
+__global__ void __launch_bounds__(256)
+    morton_rank_kernel(const float* __restrict__ q, int64_t m, MortonFrame f, uint32_t* __restrict__ bins,
+                       uint32_t* __restrict__ keys, uint32_t* __restrict__ ranks) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    const uint32_t key = morton_key<D>(q, i, f);
     keys[i] = key;
+    ranks[i] = atomicAdd(bins + key, 1u);
+}
+
+// counting sort, pass 2: id -> its bin's offset + its rank
+__global__ void __launch_bounds__(256)
+    morton_scatter_kernel(int64_t m, const uint32_t* __restrict__ offs, const uint32_t* __restrict__ keys,
+                          const uint32_t* __restrict__ ranks, uint32_t* __restrict__ ids) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    ids[__ldg(offs + __ldg(keys + i)) + __ldg(ranks + i)] = uint32_t(i);
+}
+
+namespace {
+constexpr size_t kAlign = 256;
+size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+int64_t key_bins(int dim) { return int64_t(1) << (morton_bits_per_dim(dim) * dim); }
+bool use_counting(int64_t m, int dim) {
+    static const int64_t min_m = [] {  // experiment knob: 0 = never
+        const char* e = std::getenv("FKD_COUNT_SORT_MIN");
+        return e ? std::atoll(e) : int64_t(1) << 20;
+    }();
+    return min_m > 0 && m >= min_m && dim >= 1 && dim <= 8 && m < (int64_t(1) << 32);
+}
+size_t scan_bytes(int64_t bins) {
+    size_t bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)bins);
+    return bytes;
+}
+}  // namespace
+
+// radix path: keys + ids for the onesweep
+template <int D>
+__global__ void __launch_bounds__(256)
+    morton_keys_kernel(const float* __restrict__ q, int64_t m, MortonFrame f,
+                       uint32_t* __restrict__ keys, uint32_t* __restrict__ ids) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    keys[i] = morton_key<D>(q, i, f);
     ids[i] = uint32_t(i);
 }
 
-size_t morton_temp_bytes(int64_t m) {
+size_t morton_temp_bytes(int64_t m, int dim) {
     size_t bytes = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr,
                                     (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)m, 0, 32);
+    if (use_counting(m, dim)) {
+        const int64_t bins = key_bins(dim);
+        bytes = std::max(bytes, 2 * align_up(size_t(bins) * sizeof(uint32_t)) + scan_bytes(bins));
+    }
     return bytes;
 }
 
@@ -61,6 +121,26 @@ int morton_order(const float* d_queries, int64_t m, int dim, const MortonFrame& 
                  uint32_t* keys_in, uint32_t* keys_out, uint32_t* ids_in, uint32_t* ids_out,
                  void* temp, size_t temp_bytes, cudaStream_t st) {
     const unsigned grid = unsigned((m + 255) / 256);
+    if (use_counting(m, dim)) {
+        const int64_t bins = key_bins(dim);
+        if (bins != (int64_t(1) << (f.bits * dim))) return -1;
+        uint32_t* cnt = static_cast<uint32_t*>(temp);
+        uint32_t* offs = reinterpret_cast<uint32_t*>(static_cast<char*>(temp) + align_up(size_t(bins) * 4));
+        void* stmp = static_cast<char*>(temp) + 2 * align_up(size_t(bins) * 4);
+        size_t sbytes = scan_bytes(bins);
+        if (2 * align_up(size_t(bins) * 4) + sbytes > temp_bytes) return -1;
+        if (cudaMemsetAsync(cnt, 0, size_t(bins) * 4, st) != cudaSuccess) return -1;
+        uint32_t* ranks = keys_out;
+        switch (dim) {
+#define FKD_RANK(D) case D: morton_rank_kernel<D><<<grid, 256, 0, st>>>(d_queries, m, f, cnt, keys_in, ranks); break;
+            FKD_RANK(1) FKD_RANK(2) FKD_RANK(3) FKD_RANK(4) FKD_RANK(5) FKD_RANK(6) FKD_RANK(7) FKD_RANK(8)
+#undef FKD_RANK
+            default: return -1;
+        }
+        if (cub::DeviceScan::ExclusiveSum(stmp, sbytes, cnt, offs, (int)bins, st) != cudaSuccess) return -1;
+        morton_scatter_kernel<<<grid, 256, 0, st>>>(m, offs, keys_in, ranks, ids_out);
+        return 2;  // our own launches (the scan is a library launch)
+    }
     switch (dim) {
         case 1: morton_keys_kernel<1><<<grid, 256, 0, st>>>(d_queries, m, f, keys_in, ids_in); break;
         case 2: morton_keys_kernel<2><<<grid, 256, 0, st>>>(d_queries, m, f, keys_in, ids_in); break;

@@ -15,8 +15,8 @@ struct MortonFrame {
 };
 
 int morton_bits_per_dim(int dim);
-size_t morton_temp_bytes(int64_t m);
-// Keys + radix sort; ids_out receives the walk order.  Returns launches or -1.
+size_t morton_temp_bytes(int64_t m, int dim);
+// Keys + counting or radix sort; ids_out receives the walk order.  Returns launches or -1.
 int morton_order(const float* d_queries, int64_t m, int dim, const MortonFrame& f,
                  uint32_t* keys_in, uint32_t* keys_out, uint32_t* ids_in, uint32_t* ids_out,
                  void* temp, size_t temp_bytes, cudaStream_t st);

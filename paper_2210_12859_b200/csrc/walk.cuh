@@ -152,17 +152,24 @@ __device__ __forceinline__ void load_point(const float* __restrict__ nodes, int3
     }
 }
 
+// Sorted insertion of x into L (ascending; x < L[KB-1], so the last key
+// drops out).  All KB compares are independent, then each slot takes its
+// left neighbour (x went further left), x (x lands here) or stays:
+//   L[j] = c[j-1] ? L[j-1] : (c[j] ? x : L[j]),   c[j] = x < L[j],
+// which is 6 SASS per slot at depth 3.  (A compare-exchange bubble is a
+// serial chain through all slots; ptxas shortens it with a second compare
+// per slot, 8 SASS per slot — measured in the kNN8 walk, where insertions
+// are a third of all instructions.)  c is monotone because L is sorted;
+// keys are distinct except equal dummies / empty slots, which x never
+// equals (x > 0 = dummy, x < L[KB-1] <= the empty key).
 template <int KB>
 __device__ __forceinline__ void list_insert(uint64_t (&L)[KB], uint64_t x) {
-    // one 64-bit compare per slot feeds both selects (the compiler otherwise
-    // evaluates L < x and x < L separately: 4 ISETP instead of 2)
+    bool c[KB];
 #pragma unroll
-    for (int j = 0; j < KB; ++j) {
-        const uint64_t Lj = L[j];
-        const bool keep = Lj < x;
-        L[j] = keep ? Lj : x;
-        x = keep ? x : Lj;
-    }
+    for (int j = 0; j < KB; ++j) c[j] = x < L[j];
+#pragma unroll
+    for (int j = KB - 1; j > 0; --j) L[j] = c[j] ? (c[j - 1] ? L[j - 1] : x) : L[j];
+    L[0] = c[0] ? x : L[0];
 }
 
 template <bool STATS>
@@ -440,6 +447,13 @@ __device__ __forceinline__ void add_totals(const WalkArgs& a, unsigned long long
 #ifndef FKD_MINB_KB16
 #define FKD_MINB_KB16 1
 #endif
+// Threads per walk block: a block's slot stays held until its slowest warp
+// ends, so smaller blocks waste less occupancy on budget-capped stragglers.
+#ifndef FKD_WALK_T
+#define FKD_WALK_T 256
+#endif
+constexpr int kWalkThreads = FKD_WALK_T;
+
 template <int KB>
 constexpr int walk_min_blocks() {
     return KB == 8 ? FKD_MINB_KB8 : (KB == 16 ? FKD_MINB_KB16 : 1);
@@ -447,7 +461,7 @@ constexpr int walk_min_blocks() {
 
 // One thread per walk position (plain grid).
 template <int D, int S, int KB, bool STATS, bool UNORDERED>
-__global__ void __launch_bounds__(256, walk_min_blocks<KB>()) walk_kernel(const WalkArgs a) {
+__global__ void __launch_bounds__(kWalkThreads, walk_min_blocks<KB>()) walk_kernel(const WalkArgs a) {
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     LaneWalk<D, S, KB, STATS, UNORDERED> w;
     bool active = i < a.m && w.init(a, i);

@@ -43,7 +43,7 @@ void launch_overflow(const WalkArgs& a, cudaStream_t st) {
 
 template <int D, int S, int KB, bool STATS, bool UNORDERED>
 void launch_one(const WalkArgs& a, cudaStream_t st) {
-    walk_kernel<D, S, KB, STATS, UNORDERED><<<walk_blocks(a.m, 256), 256, 0, st>>>(a);
+    walk_kernel<D, S, KB, STATS, UNORDERED><<<walk_blocks(a.m, kWalkThreads), kWalkThreads, 0, st>>>(a);
 }
 
 template <int D, int S, int KB, bool UNORDERED>

@@ -34,7 +34,9 @@ def main():
     dq = torch.from_numpy(qs).cuda()
     cfgs = {"fcp": (fk.QueryKind.fcp, 1, float("inf")), "knn8": (fk.QueryKind.knn, 8, float("inf")),
             "knn8r01": (fk.QueryKind.knn, 8, 0.01), "knn16": (fk.QueryKind.knn, 16, float("inf")),
-            "knn4": (fk.QueryKind.knn, 4, float("inf")), "knn50": (fk.QueryKind.knn, 50, float("inf"))}
+            "knn4": (fk.QueryKind.knn, 4, float("inf")), "knn50": (fk.QueryKind.knn, 50, float("inf")),
+            "knn20": (fk.QueryKind.knn, 20, float("inf")), "knn32": (fk.QueryKind.knn, 32, float("inf")),
+            "knn64": (fk.QueryKind.knn, 64, float("inf"))}
     for name in args.configs.split(","):
         kind, k, r = cfgs[name]
         counts = torch.empty(args.m, dtype=torch.int32, device="cuda")
