@@ -152,21 +152,36 @@ __device__ __forceinline__ void load_point(const float* __restrict__ nodes, int3
     }
 }
 
+// Key order on the FP64 compare.  A key is ((bits(d2) + 1) << 32) | node
+// with d2 in [0, +inf] (queries and tree are finite; cap2 is not NaN), so its
+// sign bit is 0 and its high word is <= 0x7F800001: read as an IEEE double it
+// is finite and non-negative, and non-negative doubles order exactly like
+// their bit patterns (FP64 never flushes subnormals; +0 is only the dummy
+// key 0).  One DSETP replaces the two-instruction 64-bit ISETP pair and runs
+// on the FP64 pipe instead of the ALU pipe the walk saturates; and since the
+// selects that follow are integer, ptxas cannot re-form a min/max idiom with
+// compares of its own.  (B200-specific: sm_100 has a full-rate-class FP64
+// pipe.)
+__device__ __forceinline__ bool key_lt(uint64_t a, uint64_t b) {
+    return __longlong_as_double(static_cast<long long>(a)) < __longlong_as_double(static_cast<long long>(b));
+}
+
 // Sorted insertion of x into L (ascending; x < L[KB-1], so the last key
 // drops out).  All KB compares are independent, then each slot takes its
 // left neighbour (x went further left), x (x lands here) or stays:
-//   L[j] = c[j-1] ? L[j-1] : (c[j] ? x : L[j]),   c[j] = x < L[j],
-// which is 6 SASS per slot at depth 3.  (A compare-exchange bubble is a
-// serial chain through all slots; ptxas shortens it with a second compare
-// per slot, 8 SASS per slot — measured in the kNN8 walk, where insertions
-// are a third of all instructions.)  c is monotone because L is sorted;
-// keys are distinct except equal dummies / empty slots, which x never
-// equals (x > 0 = dummy, x < L[KB-1] <= the empty key).
+//   L[j] = c[j] ? (c[j-1] ? L[j-1] : x) : L[j],   c[j] = x < L[j],
+// one DSETP + a predicated SEL pair per slot (KB = 8: 24 SASS).  (The
+// compare-exchange bubble is a serial chain through all slots, which ptxas
+// shortened with a second 64-bit compare per slot: 61 SASS for KB = 8,
+// measured in the kNN8 walk, where insertions were a third of all
+// instructions.)  c is monotone because L is sorted; keys are distinct
+// except equal dummies / empty slots, which x never equals (x > 0 = dummy,
+// x < L[KB-1] <= the empty key).
 template <int KB>
 __device__ __forceinline__ void list_insert(uint64_t (&L)[KB], uint64_t x) {
     bool c[KB];
 #pragma unroll
-    for (int j = 0; j < KB; ++j) c[j] = x < L[j];
+    for (int j = 0; j < KB; ++j) c[j] = key_lt(x, L[j]);
 #pragma unroll
     for (int j = KB - 1; j > 0; --j) L[j] = c[j] ? (c[j - 1] ? L[j - 1] : x) : L[j];
     L[0] = c[0] ? x : L[0];
@@ -274,14 +289,14 @@ struct LaneWalk {
             // on a first visit.
             const float d2 = sq_dist(q, p);
             const uint64_t key = make_key(d2, curr);
-            if (from_parent && key < L[KB - 1]) {  // d2 <= cap2 and beats the kth (cap_key)
+            if (from_parent && key_lt(key, L[KB - 1])) {  // d2 <= cap2 and beats the kth (cap_key)
                 list_insert(L, key);
                 r2 = key_dist(L[KB - 1]);
             }
         } else if (from_parent) {  // fcp: a branch is cheaper than 8 more FP ops
             const float d2 = sq_dist(q, p);
             const uint64_t key = make_key(d2, curr);
-            if (key < L[KB - 1]) {  // d2 <= cap2 and beats the best (cap_key)
+            if (key_lt(key, L[KB - 1])) {  // d2 <= cap2 and beats the best (cap_key)
                 list_insert(L, key);
                 r2 = key_dist(L[KB - 1]);
             }
