@@ -87,6 +87,8 @@ typedef struct fkd_timings {
     float tail_ms;    /* of walk_ms: the overflow pass for over-budget queries   */
     int32_t launches; /* kernels this library launched for the call             */
     int32_t walk_launches;
+    int64_t overflowed; /* queries that left the walk kernel over its step budget
+                           (last sub-batch of <= 2^30 queries)                    */
 } fkd_timings;
 
 typedef struct fkd_tree fkd_tree;

@@ -311,7 +311,7 @@ def run_batch_device(tree: KdTree, queries, counts, hits, options: Optional[Batc
     tdict = None
     if timings:
         tdict = {"order_ms": tm.order_ms, "walk_ms": tm.walk_ms, "tail_ms": tm.tail_ms, "launches": tm.launches,
-                 "walk_launches": tm.walk_launches}
+                 "walk_launches": tm.walk_launches, "overflowed": tm.overflowed}
     return QueryStats.from_c(st), tdict
 
 

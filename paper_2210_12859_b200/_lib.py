@@ -32,7 +32,7 @@ class fkd_query_stats(C.Structure):
 
 class fkd_timings(C.Structure):
     _fields_ = [("order_ms", C.c_float), ("walk_ms", C.c_float), ("tail_ms", C.c_float), ("launches", C.c_int32),
-                ("walk_launches", C.c_int32)]
+                ("walk_launches", C.c_int32), ("overflowed", C.c_int64)]
 
 
 def _load() -> C.CDLL:

@@ -747,7 +747,7 @@ fkd_status fkd_run_batch_device(const fkd_tree* t, const float* d_q, int64_t m, 
     fkd_status s = validate(t, m, dim, o, &cap2);
     if (s != FKD_OK) return s;
     if (stats) *stats = fkd_query_stats{0, 0, 0};
-    if (timings) *timings = fkd_timings{0.0f, 0.0f, 0.0f, 0, 0};
+    if (timings) *timings = fkd_timings{0.0f, 0.0f, 0.0f, 0, 0, 0};
     if (m == 0) return FKD_OK;
     if (t->reps.empty()) return fail(FKD_NO_DEVICE, "tree has no device replica");
     if ((reinterpret_cast<uintptr_t>(d_hits) & 7u) != 0)
@@ -781,6 +781,7 @@ fkd_status fkd_run_batch_device(const fkd_tree* t, const float* d_q, int64_t m, 
             cudaEventElapsedTime(&timings->tail_ms, w->ev[3], w->ev[2]);
             timings->launches = launches;
             timings->walk_launches = walk_launches;
+            timings->overflowed = int64_t(w->h_small[5]);
         }
         return FKD_OK;
     };

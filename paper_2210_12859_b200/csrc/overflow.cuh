@@ -19,7 +19,12 @@
 //      each with its own register list, all pruning against min(own kth,
 //      shared r2) where the shared r2 is the smallest kth distance any
 //      thread has seen (atomicMin on the float bits, valid for d2 >= 0);
-//   4. merge  — k rounds of a block-wide min over the threads' list heads.
+//   4. select — the final set lies within the shared bound (any thread's kth
+//      distance bounds the final kth from above), so the list entries <= it
+//      are compacted into shared memory and, when at most kRankMax survive,
+//      each computes its rank among them (distinct keys) and lands in its
+//      output slot directly: two barriers instead of 2k.  Otherwise, k rounds
+//      of a block-wide min over the threads' list heads.
 //
 // Exactness: the answer is the k smallest admissible keys under hit_order;
 // every pruning bound used is >= the final kth distance and comparisons stay
@@ -34,6 +39,7 @@
 namespace fkd {
 
 constexpr int kOvfFrontierMax = 4096;
+constexpr int kRankMax = 1024;  // rank selection's candidate cap (C^2 / THREADS compares per thread)
 
 template <int KB>
 __device__ __forceinline__ uint64_t list_head(const uint64_t (&L)[KB], int dummies) {
@@ -60,6 +66,7 @@ __global__ void __launch_bounds__(THREADS) overflow_kernel(const WalkArgs a) {
     __shared__ int work_next;
     __shared__ unsigned long long red[THREADS / 32];
     __shared__ unsigned long long winner;
+    __shared__ int ccount;
 
     const int tid = threadIdx.x;
     const int32_t n = a.n;
@@ -168,34 +175,65 @@ __global__ void __launch_bounds__(THREADS) overflow_kernel(const WalkArgs a) {
         }
         __syncthreads();
 
-        // ---- 4. block-wide k-way merge of the sorted lists
-        for (int j = 0; j < k; ++j) {
-            uint64_t h = list_head(L, dummies);
-            uint64_t m = h;
-            for (int off = 16; off > 0; off >>= 1) {
-                const uint64_t o = __shfl_xor_sync(0xffffffffu, m, off);
-                m = o < m ? o : m;
+        // ---- 4a. rank selection among the entries within the final bound
+        if (tid == 0) ccount = 0;
+        __syncthreads();
+        // frontier[] is free now; it holds kRankMax 64-bit candidates
+        uint64_t* cand = reinterpret_cast<uint64_t*>(&frontier[0][0]);
+        static_assert(sizeof(frontier) >= kRankMax * sizeof(uint64_t), "candidate buffer");
+        const float fb = __uint_as_float(r2_bits);
+#pragma unroll
+        for (int j = 0; j < KB; ++j) {
+            if (j >= dummies && L[j] != kEmptyKey && key_dist(L[j]) <= fb) {
+                const int pos = atomicAdd(&ccount, 1);
+                if (pos < kRankMax) cand[pos] = L[j];
             }
-            if ((tid & 31) == 0) red[tid >> 5] = m;
+        }
+        __syncthreads();
+        const int C = ccount;
+        if (C <= kRankMax) {
+            for (int i = tid; i < C; i += THREADS) {
+                const uint64_t x = cand[i];
+                int rank = 0;
+                for (int j = 0; j < C; ++j) rank += key_lt(cand[j], x);
+                if (rank < k)
+                    reinterpret_cast<int2*>(a.hits + qi * k)[rank] =
+                        make_int2(int32_t(uint32_t(x)), int32_t(uint32_t(x >> 32) - 1u));
+            }
+            for (int j = C + tid; j < k; j += THREADS)  // fewer than k admissible: Hit{-1, +inf}
+                reinterpret_cast<int2*>(a.hits + qi * k)[j] = make_int2(-1, 0x7f800000);
+            if (tid == 0) fcount[0] = C < k ? C : k;
             __syncthreads();
-            if (tid < 32) {
-                uint64_t v = tid < THREADS / 32 ? red[tid] : kEmptyKey;
+        } else {
+            // ---- 4b. block-wide k-way merge of the sorted lists
+            for (int j = 0; j < k; ++j) {
+                uint64_t h = list_head(L, dummies);
+                uint64_t m = h;
                 for (int off = 16; off > 0; off >>= 1) {
-                    const uint64_t o = __shfl_xor_sync(0xffffffffu, v, off);
-                    v = o < v ? o : v;
+                    const uint64_t o = __shfl_xor_sync(0xffffffffu, m, off);
+                    m = o < m ? o : m;
                 }
-                if (tid == 0) winner = v;
+                if ((tid & 31) == 0) red[tid >> 5] = m;
+                __syncthreads();
+                if (tid < 32) {
+                    uint64_t v = tid < THREADS / 32 ? red[tid] : kEmptyKey;
+                    for (int off = 16; off > 0; off >>= 1) {
+                        const uint64_t o = __shfl_xor_sync(0xffffffffu, v, off);
+                        v = o < v ? o : v;
+                    }
+                    if (tid == 0) winner = v;
+                }
+                __syncthreads();
+                const uint64_t w = winner;
+                if (h == w && w != kEmptyKey) list_pop(L, dummies);
+                if (tid == 0) {
+                    reinterpret_cast<int2*>(a.hits + qi * k)[j] =
+                        make_int2(int32_t(uint32_t(w)), int32_t(uint32_t(w >> 32) - 1u));
+                    if (j == 0) fcount[0] = 0;
+                    if (w != kEmptyKey) ++fcount[0];  // reuse as the hit counter
+                }
+                __syncthreads();
             }
-            __syncthreads();
-            const uint64_t w = winner;
-            if (h == w && w != kEmptyKey) list_pop(L, dummies);
-            if (tid == 0) {
-                reinterpret_cast<int2*>(a.hits + qi * k)[j] =
-                    make_int2(int32_t(uint32_t(w)), int32_t(uint32_t(w >> 32) - 1u));
-                if (j == 0) fcount[0] = 0;
-                if (w != kEmptyKey) ++fcount[0];  // reuse as the hit counter
-            }
-            __syncthreads();
         }
         if (tid == 0) a.counts[qi] = fcount[0];
         __syncthreads();

@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--clustered", action="store_true")
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--configs", default="fcp,knn8,knn8r01")
+    ap.add_argument("--sorted-only", action="store_true")
     args = ap.parse_args()
     gen = (lambda s, c: fk.clustered_points(1, s, c, args.dim)) if args.clustered else \
         (lambda s, c: fk.random_points(1, s, c, args.dim))
@@ -41,21 +42,22 @@ def main():
         kind, k, r = cfgs[name]
         counts = torch.empty(args.m, dtype=torch.int32, device="cuda")
         hits = torch.empty(args.m * k, dtype=torch.int64, device="cuda")
-        for morton in (True, False):
+        for morton in ((True,) if args.sorted_only else (True, False)):
             opt = fk.BatchOptions(kind=kind, k=k, max_radius=r, morton=morton)
             fk.run_batch_device(tree, dq, counts, hits, opt)
-            walk, order, tail = [], [], []
+            walk, order, tail, ovf = [], [], [], 0
             for _ in range(args.reps):
                 _, tm = fk.run_batch_device(tree, dq, counts, hits, opt, timings=True)
                 walk.append(tm["walk_ms"])
                 order.append(tm["order_ms"])
                 tail.append(tm["tail_ms"])
+                ovf = tm["overflowed"]
             st, _ = fk.run_batch_device(tree, dq, counts, hits,
                                         fk.BatchOptions(kind=kind, k=k, max_radius=r, morton=morton,
                                                         collect_stats=True))
             w = float(np.median(walk))
             o = float(np.median(order))
-            print(json.dumps({"cfg": name, "morton": morton, "walk_ms": round(w, 3), "order_ms": round(o, 3), "tail_ms": round(float(np.median(tail)), 3),
+            print(json.dumps({"cfg": name, "morton": morton, "walk_ms": round(w, 3), "order_ms": round(o, 3), "tail_ms": round(float(np.median(tail)), 3), "overflowed": ovf,
                               "walk_qps": round(args.m / w * 1e3 / 1e6, 1), "total_qps_M": round(args.m / (w + o) * 1e3 / 1e6, 1),
                               "P": st.nodes_processed / args.m, "steps": st.steps / args.m}), flush=True)
 
