@@ -44,12 +44,14 @@ struct Tuning {
     int budget = -1;  // -1: per kind (measured on C3: fcp 1024, kNN 3072 loop trips)
     int wave = 0;
     std::vector<int> rounds{64, 64, 128, 256, 512, 1024};
-    int64_t resume_min = 0;  // 0: SMs x 2048
+    int64_t resume_min = 0;  // 0: SMs x 64 (measured: 8-D and 4-D kNN64 tails; C3's ~2k stay on the CTA pass)
+    int resume_trips = 0;    // 0: 4 x budget (measured: 8-D fcp 4096, kNN8/16 12288 best); <0: unbounded
 };
 
 // Launch tuning, overridable per call for experiments and tests:
 // FKD_BUDGET=<loop trips before the overflow pass; <0 per kind, 0 off>,
 // FKD_RESUME_MIN=<overflow count that selects the resume pass>,
+// FKD_RESUME_TRIPS=<steps the resume pass adds before the CTA pass; <0 unbounded>,
 // FKD_WAVE=1 + FKD_ROUNDS=<t1,t2,..> (wave rounds, off: measured slower).
 Tuning tuning() {
     return [] {
@@ -57,6 +59,7 @@ Tuning tuning() {
         if (const char* e = std::getenv("FKD_BUDGET")) x.budget = std::atoi(e);  // <0: per kind, 0: off
         if (const char* e = std::getenv("FKD_WAVE")) x.wave = std::atoi(e) != 0;
         if (const char* e = std::getenv("FKD_RESUME_MIN")) x.resume_min = std::atoll(e);
+        if (const char* e = std::getenv("FKD_RESUME_TRIPS")) x.resume_trips = std::atoi(e);
         if (const char* e = std::getenv("FKD_ROUNDS")) {  // e.g. "64,64,128"
             x.rounds.clear();
             for (const char* p = e; *p;) {
@@ -344,7 +347,7 @@ fkd_status enqueue(const fkd_tree* t, Replica& r, Workspace* w, const float* d_q
             int dev = 0, sms = 0;
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            a.resume_min = tu.resume_min > 0 ? tu.resume_min : int64_t(sms) * 2048;
+            a.resume_min = tu.resume_min > 0 ? tu.resume_min : int64_t(sms) * 64;
         }
         if (sort) {
             const int64_t half = w->key_cap / 2;
@@ -383,6 +386,7 @@ fkd_status enqueue(const fkd_tree* t, Replica& r, Workspace* w, const float* d_q
             }
             a.ovf_ids = const_cast<uint32_t*>(a.wave_in);
             a.ovf_count = const_cast<unsigned long long*>(a.wave_n_in);
+            a.resume_min = 0;  // the overflow pass takes every survivor
         } else {
             nl = launch_walk(a, t->dim, t->stride, stats, unordered, 0, st);
             if (nl <= 0) return fail(FKD_CUDA_ERROR, "no kernel for this configuration");
@@ -390,12 +394,15 @@ fkd_status enqueue(const fkd_tree* t, Replica& r, Workspace* w, const float* d_q
             if (a.budget > 0) {
                 // resume pass: continues the parked walks with the plain grid
                 // when at least resume_min overflowed (decided on the device)
+                // for at most resume_trips more steps; its survivors (parked
+                // again) are the CTA pass's list
+                FKD_CUDA(cudaMemsetAsync(w->small + 8, 0, sizeof(unsigned long long), st));
+                a.wave_out = w->wave_ids;
+                a.wave_n_out = w->small + 8;
                 WalkArgs r = a;
-                r.trips = 0x7fffffff;
+                r.trips = tu.resume_trips > 0 ? tu.resume_trips : (tu.resume_trips < 0 ? 0x7fffffff : 4 * a.budget);
                 r.wave_in = a.ovf_ids;
                 r.wave_n_in = a.ovf_count;
-                r.wave_out = w->wave_ids;
-                r.wave_n_out = w->small + 8;
                 nl += launch_walk(r, t->dim, t->stride, stats, unordered, 2, st);
                 FKD_CUDA(cudaGetLastError());
             }

@@ -74,14 +74,17 @@ __global__ void __launch_bounds__(THREADS) overflow_kernel(const WalkArgs a) {
     const int dummies = KB - k;
     const float cap2 = a.cap2;
 
-    // many over-budget queries were finished by the resume pass instead
-    if (a.resume_min > 0 && *a.ovf_count >= (unsigned long long)a.resume_min) return;
+    // many over-budget queries: the resume pass continued them, and this
+    // pass takes the ones that outlived it
+    const bool resumed = a.resume_min > 0 && *a.ovf_count >= (unsigned long long)a.resume_min;
+    const uint32_t* ids = resumed ? a.wave_out : a.ovf_ids;
+    const unsigned long long count = resumed ? *a.wave_n_out : *a.ovf_count;
     while (true) {
         if (tid == 0) slot = atomicAdd(a.ovf_next, 1ull);
         __syncthreads();
         const unsigned long long s = slot;
-        if (s >= *a.ovf_count) return;
-        const int64_t qi = a.ovf_ids[s];
+        if (s >= count) return;
+        const int64_t qi = ids[s];
 
         float q[D];
 #pragma unroll

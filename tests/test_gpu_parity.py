@@ -196,15 +196,23 @@ def test_cpp_shim_against_reference():
     assert "OK" in out.stdout
 
 
-@pytest.mark.parametrize("budget,resume_min", [("1", "0"), ("3", "0"), ("50", "0"), ("2", "1"), ("40", "1")])
-def test_overflow_pass_is_exact(oracle, budget, resume_min, monkeypatch):
+@pytest.mark.parametrize("budget,resume_min,resume_trips", [
+    ("1", "0", "0"), ("3", "0", "0"), ("50", "0", "0"),   # CTA pass only (few overflow)
+    ("2", "1", "-1"), ("40", "1", "-1"),                   # unbounded resume pass
+    ("2", "1", "3"), ("5", "1", "40"), ("40", "1", "0"),   # budgeted resume, survivors -> CTA pass
+])
+def test_overflow_pass_is_exact(oracle, budget, resume_min, resume_trips, monkeypatch):
     """Queries stopped by the walk budget are finished by the CTA-per-query
     overflow pass (overflow.cuh) or, when many overflow (FKD_RESUME_MIN=1
     forces it), resumed from their parked (curr, prev) by the plain-grid resume
-    pass; results must stay bit-exact either way."""
+    pass for FKD_RESUME_TRIPS more steps, whose survivors are parked again and
+    handed to the CTA pass; results must stay bit-exact in every combination."""
     monkeypatch.setenv("FKD_BUDGET", budget)
+    monkeypatch.setenv("FKD_RESUME_TRIPS", resume_trips)
     if resume_min != "0":
         monkeypatch.setenv("FKD_RESUME_MIN", resume_min)
+    else:
+        monkeypatch.setenv("FKD_RESUME_MIN", str(1 << 40))
     rng = oracle.instance_rng(777)
     for t in range(24):
         n = rng.next_int(1, 6000)
