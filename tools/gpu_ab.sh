@@ -1,4 +1,7 @@
-python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-python tools/quickbench.py --sorted-only --clustered --configs fcp,knn8,knn16 --reps 2 2>&1 | grep true
-python tools/quickbench.py --sorted-only --dim 4 --m 2000000 --configs knn50,knn64 --reps 2 2>&1 | grep true
-python tools/quickbench.py --sorted-only --dim 8 --n 1000000 --m 200000 --configs fcp,knn8,knn16 --reps 2 2>&1 | grep true
+for o in morton tree; do echo "order $o"; export FKD_ORDER=$o
+python tools/quickbench.py --sorted-only --configs fcp,knn8 --reps 3 2>&1 | grep true
+python tools/quickbench.py --sorted-only --clustered --configs fcp,knn8 --reps 3 2>&1 | grep true
+python tools/quickbench.py --sorted-only --dim 4 --m 2000000 --configs fcp,knn8 --reps 3 2>&1 | grep true
+python tools/quickbench.py --sorted-only --dim 2 --configs fcp,knn16 --reps 3 2>&1 | grep true
+done
+FKD_ORDER=tree python -m pytest tests -m gpu -x -q -k "golden or hash or fuzz or dims" 2>&1 | tail -2
