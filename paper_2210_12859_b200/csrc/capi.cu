@@ -97,8 +97,9 @@ struct Workspace {
     cudaStream_t stream = nullptr;  // own stream (host path)
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     // host path: this slot's last H2D / walk / D2H completion (timing disabled)
-    cudaEvent_t pe[3] = {nullptr, nullptr, nullptr};
+    cudaEvent_t pe[4] = {nullptr, nullptr, nullptr, nullptr};  // [3]: walk -> tail stream hand-off
     cudaStream_t cin = nullptr, cout = nullptr;  // copy streams (first slot of a call)
+    cudaStream_t tail = nullptr;                 // high-priority stream for the tail passes
     uint32_t* keys = nullptr;       // [2 * cap] keys in/out
     uint32_t* ids = nullptr;        // [2 * cap] ids in/out
     int64_t key_cap = 0;
@@ -138,6 +139,7 @@ struct Workspace {
         for (auto& e : pe)
             if (e) cudaEventDestroy(e);
         if (cin) cudaStreamDestroy(cin);
+        if (tail) cudaStreamDestroy(tail);
         if (cout) cudaStreamDestroy(cout);
         if (stream) cudaStreamDestroy(stream);
     }
@@ -218,6 +220,11 @@ fkd_status acquire_ws(Replica& r, Workspace** out) {
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&w->cin, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&w->cout, cudaStreamNonBlocking);
+    if (e == cudaSuccess) {
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        e = cudaStreamCreateWithPriority(&w->tail, cudaStreamNonBlocking, hi);
+    }
     if (e == cudaSuccess) e = cudaMalloc(&w->small, 16 * sizeof(unsigned long long));
     if (e == cudaSuccess) e = cudaMallocHost(&w->h_small, 16 * sizeof(unsigned long long));
     if (e != cudaSuccess) {
@@ -284,7 +291,7 @@ fkd_status enqueue(const fkd_tree* t, Replica& r, Workspace* w, const float* d_q
                    const fkd_batch_options* o, float cap2, int32_t* d_counts, fkd_hit* d_hits,
                    fkd_query_stats* d_per_query, bool stats, cudaStream_t st, int* launches,
                    int* walk_launches, cudaEvent_t ev_mid, cudaEvent_t ev_tail = nullptr,
-                   int64_t id_offset = 0) {
+                   int64_t id_offset = 0, cudaStream_t tail_st = nullptr, int budget_div = 1) {
     const int k = o->kind == FKD_KNN ? o->k : 1;
     if (t->n == 0) {  // every query returns empty; queries are not read (batch.cpp:75)
         *launches += fill_empty(d_counts, d_hits, m, k, st);
@@ -332,7 +339,8 @@ fkd_status enqueue(const fkd_tree* t, Replica& r, Workspace* w, const float* d_q
         a.bad = w->small;
         a.id_base = id_offset + base;
         const Tuning tu = tuning();
-        const int budget = tu.budget >= 0 ? tu.budget : (k == 1 ? 1024 : 3072);
+        int budget = tu.budget >= 0 ? tu.budget : (k == 1 ? 1024 : 3072);
+        if (budget_div > 1 && budget > 0) budget = std::max(64, budget / budget_div);
         a.budget = (stats || walk_bucket_of(k) == 0 || t->dim > 8) ? 0 : budget;
         if (a.budget > 0) {
             FKD_CUDA(grow(w->ovf, w->ovf_cap, cm));
@@ -391,25 +399,38 @@ fkd_status enqueue(const fkd_tree* t, Replica& r, Workspace* w, const float* d_q
             nl = launch_walk(a, t->dim, t->stride, stats, unordered, 0, st);
             if (nl <= 0) return fail(FKD_CUDA_ERROR, "no kernel for this configuration");
             FKD_CUDA(cudaGetLastError());
+            if (a.budget > 0 && tail_st) {
+                // the tail passes run on a high-priority stream so that, in a
+                // pipeline of concurrent chunks, they take SM slots as soon as
+                // blocks retire instead of queueing behind the next chunks' walks
+                FKD_CUDA(cudaEventRecord(w->pe[3], st));
+                FKD_CUDA(cudaStreamWaitEvent(tail_st, w->pe[3], 0));
+            }
+            const cudaStream_t ts = (a.budget > 0 && tail_st) ? tail_st : st;
             if (a.budget > 0) {
                 // resume pass: continues the parked walks with the plain grid
                 // when at least resume_min overflowed (decided on the device)
                 // for at most resume_trips more steps; its survivors (parked
                 // again) are the CTA pass's list
-                FKD_CUDA(cudaMemsetAsync(w->small + 8, 0, sizeof(unsigned long long), st));
+                FKD_CUDA(cudaMemsetAsync(w->small + 8, 0, sizeof(unsigned long long), ts));
                 a.wave_out = w->wave_ids;
                 a.wave_n_out = w->small + 8;
                 WalkArgs r = a;
                 r.trips = tu.resume_trips > 0 ? tu.resume_trips : (tu.resume_trips < 0 ? 0x7fffffff : 4 * a.budget);
                 r.wave_in = a.ovf_ids;
                 r.wave_n_in = a.ovf_count;
-                nl += launch_walk(r, t->dim, t->stride, stats, unordered, 2, st);
+                nl += launch_walk(r, t->dim, t->stride, stats, unordered, 2, ts);
                 FKD_CUDA(cudaGetLastError());
             }
         }
-        if (ev_tail && base == 0) FKD_CUDA(cudaEventRecord(ev_tail, st));
-        const int tail = launch_walk(a, t->dim, t->stride, stats, unordered, 1, st);  // overflow pass
+        const cudaStream_t ts = (a.budget > 0 && tail_st && !wave) ? tail_st : st;
+        if (ev_tail && base == 0) FKD_CUDA(cudaEventRecord(ev_tail, ts));
+        const int tail = launch_walk(a, t->dim, t->stride, stats, unordered, 1, ts);  // overflow pass
         FKD_CUDA(cudaGetLastError());
+        if (ts != st) {
+            FKD_CUDA(cudaEventRecord(w->pe[3], ts));
+            FKD_CUDA(cudaStreamWaitEvent(st, w->pe[3], 0));
+        }
         *launches += nl + tail;
         *walk_launches += nl + tail;
     }
@@ -856,6 +877,7 @@ fkd_status fkd_run_batch(const fkd_tree* t, const float* queries, int64_t m, int
         int rep;
         Workspace* w;
         int64_t base, count;
+        int64_t off;  // offset in the device's shard (full staging)
     };
     std::vector<Job> jobs;
     std::vector<std::vector<Workspace*>> wss(ndev);
@@ -870,20 +892,46 @@ fkd_status fkd_run_batch(const fkd_tree* t, const float* queries, int64_t m, int
             err = acquire_ws(*t->reps[di], &w);
             if (err == FKD_OK) wss[di].push_back(w);
         }
+        // the workspace that already holds the largest staging serves as slot 0
+        // (the pool hands workspaces out in no particular order)
+        std::stable_sort(wss[di].begin(), wss[di].end(),
+                         [](const Workspace* x, const Workspace* y) { return x->h_cap > y->h_cap; });
         int64_t b = lo;
         for (size_t c = 0; c < sizes.size() && err == FKD_OK; ++c) {
-            jobs.push_back(Job{di, wss[di][c % wss[di].size()], b, sizes[c]});
+            jobs.push_back(Job{di, wss[di][c % wss[di].size()], b, sizes[c], b - lo});
             b += sizes[c];
         }
     }
+    // Staging.  Full (default when it fits in a quarter of the free device
+    // memory): the first slot holds the whole shard's queries and results,
+    // every H2D is issued up front (so the copy-in finishes early instead of
+    // sharing the PCIe link with the copy-out: each direction drops from 55 to
+    // 44 GB/s when both run) and no chunk waits for a slot's buffers.  Ring
+    // (fallback): every slot holds its largest chunk and chunk c reuses slot
+    // c mod R's buffers after chunk c-R's walk / D2H.
+    std::vector<char> full(ndev, 0);
     if (err == FKD_OK) {
-        // size every workspace for its largest chunk before enqueueing
+        static const int full_env = [] {  // experiment knob: FKD_FULL_STAGING=0 forces the ring
+            const char* e = std::getenv("FKD_FULL_STAGING");
+            return e ? std::atoi(e) : 1;
+        }();
         for (int di = 0; di < ndev && err == FKD_OK; ++di) {
+            if (wss[di].empty()) continue;
             DeviceGuard g(t->reps[di]->device);
+            int64_t shard = 0;
+            for (const Job& j : jobs)
+                if (j.rep == di) shard += j.count;
+            size_t free_b = 0, total_b = 0;
+            cudaMemGetInfo(&free_b, &total_b);
+            Workspace* w0 = wss[di][0];
+            const int64_t have = std::min({w0->q_cap / std::max(1, dim), w0->c_cap, w0->h_cap / k});
+            const double need = double(shard) * (double(dim) * 4 + 4 + 8.0 * k);
+            full[di] = full_env != 0 && (have >= shard || need <= 0.25 * double(free_b));
             for (Workspace* w : wss[di]) {
                 int64_t big = 0;
                 for (const Job& j : jobs)
                     if (j.w == w) big = std::max(big, j.count);
+                if (full[di]) big = w == w0 ? shard : 0;
                 cudaError_t e = grow(w->q, w->q_cap, big * dim);
                 if (e == cudaSuccess) e = grow(w->counts, w->c_cap, big);
                 if (e == cudaSuccess) e = grow(w->hits, w->h_cap, big * k);
@@ -891,13 +939,28 @@ fkd_status fkd_run_batch(const fkd_tree* t, const float* queries, int64_t m, int
             }
         }
     }
+    // FKD_PIPE_TRACE=1: per-chunk H2D start/end, walk end, D2H end on stderr
+    // (development aid; timing events on every stream)
+    const bool trace = std::getenv("FKD_PIPE_TRACE") != nullptr && ndev == 1;
+    // the first chunk's walk gates the first D2H: a smaller step budget ends
+    // its slowest warps sooner (the overflow pass finishes those queries)
+    const int first_div = [] {
+        const char* e = std::getenv("FKD_FIRST_BUDGET_DIV");
+        return e ? std::max(1, std::atoi(e)) : 1;
+    }();
+    const bool tail_prio = [] {  // experiment knob: FKD_TAIL_PRIO=0 keeps the tails on the slot stream
+        const char* e = std::getenv("FKD_TAIL_PRIO");
+        return !e || std::atoi(e) != 0;
+    }();
+    std::vector<cudaEvent_t> tev(trace ? jobs.size() * 4 : 0);
+    for (auto& e : tev) cudaEventCreate(&e);
     // Enqueue, per chunk c on slot s = c mod R (a slot = one workspace: its
     // staging buffers and its compute stream):
     //   copy-in stream : wait walk(c-R) [slot's q is free] ; H2D ; record in(s)
     //   slot stream    : wait in(s), wait out(c-R) [slot's results are free] ;
     //                    order + walk ; record walk(s)
     //   copy-out stream: wait walk(s) ; D2H counts + hits ; record out(s)
-    // One H2D and one D2H stream per device keep both copy engines streaming
+    // (the two bracketed waits exist only with ring staging).  One H2D and one D2H stream per device keep both copy engines streaming
     // in chunk order without queueing an H2D behind an unrelated D2H (which
     // a per-slot H2D -> walk -> D2H stream would), and the walks of
     // neighbouring chunks overlap each other's tails on the slot streams.
@@ -918,26 +981,38 @@ fkd_status fkd_run_batch(const fkd_tree* t, const float* queries, int64_t m, int
         DeviceGuard g(r.device);
         Workspace* w = j.w;
         Workspace* io = wss[j.rep][0];
-        const bool reused = std::count_if(jobs.begin(), jobs.begin() + ji,
-                                          [&](const Job& x) { return x.w == w; }) > 0;
+        const bool ring = !full[j.rep];
+        const bool reused = ring && std::count_if(jobs.begin(), jobs.begin() + ji,
+                                                  [&](const Job& x) { return x.w == w; }) > 0;
+        float* dq = ring ? w->q : io->q + j.off * dim;
+        int32_t* dc = ring ? w->counts : io->counts + j.off;
+        fkd_hit* dh = ring ? w->hits : io->hits + j.off * k;
         int launches = 0, wl = 0;
+        auto tr = [&](int which, cudaStream_t sst) {
+            if (trace) cudaEventRecord(tev[ji * 4 + which], sst);
+        };
         auto step = [&]() -> fkd_status {
             if (reused) FKD_CUDA(cudaStreamWaitEvent(io->cin, w->pe[1], 0));
-            FKD_CUDA(cudaMemcpyAsync(w->q, queries + j.base * dim, size_t(j.count) * dim * sizeof(float),
+            tr(0, io->cin);
+            FKD_CUDA(cudaMemcpyAsync(dq, queries + j.base * dim, size_t(j.count) * dim * sizeof(float),
                                      cudaMemcpyHostToDevice, io->cin));
             FKD_CUDA(cudaEventRecord(w->pe[0], io->cin));
+            tr(1, io->cin);
             FKD_CUDA(cudaStreamWaitEvent(w->stream, w->pe[0], 0));
             if (reused) FKD_CUDA(cudaStreamWaitEvent(w->stream, w->pe[2], 0));
-            fkd_status e = enqueue(t, r, w, w->q, j.count, o, cap2, w->counts, w->hits, nullptr,
-                                   want_stats, w->stream, &launches, &wl, nullptr, nullptr, j.base);
+            fkd_status e = enqueue(t, r, w, dq, j.count, o, cap2, dc, dh, nullptr,
+                                   want_stats, w->stream, &launches, &wl, nullptr, nullptr, j.base,
+                                   tail_prio ? w->tail : nullptr, ji == 0 ? first_div : 1);
             if (e != FKD_OK) return e;
             FKD_CUDA(cudaEventRecord(w->pe[1], w->stream));
+            tr(2, w->stream);
             FKD_CUDA(cudaStreamWaitEvent(io->cout, w->pe[1], 0));
-            FKD_CUDA(cudaMemcpyAsync(counts + j.base, w->counts, size_t(j.count) * sizeof(int32_t),
+            FKD_CUDA(cudaMemcpyAsync(counts + j.base, dc, size_t(j.count) * sizeof(int32_t),
                                      cudaMemcpyDeviceToHost, io->cout));
-            FKD_CUDA(cudaMemcpyAsync(hits + j.base * k, w->hits, size_t(j.count) * k * sizeof(fkd_hit),
+            FKD_CUDA(cudaMemcpyAsync(hits + j.base * k, dh, size_t(j.count) * k * sizeof(fkd_hit),
                                      cudaMemcpyDeviceToHost, io->cout));
             FKD_CUDA(cudaEventRecord(w->pe[2], io->cout));
+            tr(3, io->cout);
             return FKD_OK;
         };
         err = step();
@@ -950,6 +1025,19 @@ fkd_status fkd_run_batch(const fkd_tree* t, const float* queries, int64_t m, int
             if (e != cudaSuccess) err = fail(FKD_CUDA_ERROR, std::string("readback: ") + cudaGetErrorString(e));
         }
     }
+    if (trace && err == FKD_OK) {
+        for (auto& e : tev) cudaEventSynchronize(e);
+        for (size_t ji = 0; ji < jobs.size(); ++ji) {
+            float a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+            cudaEventElapsedTime(&a0, tev[0], tev[ji * 4 + 0]);
+            cudaEventElapsedTime(&a1, tev[0], tev[ji * 4 + 1]);
+            cudaEventElapsedTime(&a2, tev[0], tev[ji * 4 + 2]);
+            cudaEventElapsedTime(&a3, tev[0], tev[ji * 4 + 3]);
+            std::fprintf(stderr, "chunk %zu n=%lld h2d %.3f-%.3f walk_end %.3f d2h_end %.3f\n", ji,
+                         (long long)jobs[ji].count, a0, a1, a2, a3);
+        }
+    }
+    for (auto& e : tev) cudaEventDestroy(e);
     // drain every stream even after an error, then return workspaces
     unsigned long long bad = kNoBad, tot[3] = {0, 0, 0};
     for (int di = 0; di < ndev; ++di) {

@@ -1,7 +1,1 @@
-for o in morton tree; do echo "order $o"; export FKD_ORDER=$o
-python tools/quickbench.py --sorted-only --configs fcp,knn8 --reps 3 2>&1 | grep true
-python tools/quickbench.py --sorted-only --clustered --configs fcp,knn8 --reps 3 2>&1 | grep true
-python tools/quickbench.py --sorted-only --dim 4 --m 2000000 --configs fcp,knn8 --reps 3 2>&1 | grep true
-python tools/quickbench.py --sorted-only --dim 2 --configs fcp,knn16 --reps 3 2>&1 | grep true
-done
-FKD_ORDER=tree python -m pytest tests -m gpu -x -q -k "golden or hash or fuzz or dims" 2>&1 | tail -2
+for s in 3 4; do for d in 4 6 8; do echo "streams $s div $d $(FKD_STREAMS=$s FKD_CHUNK_DIV=$d python tools/e2e_diag.py 2>&1 | grep -E 'auto')"; done; done
