@@ -20,6 +20,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 
 #include <cstdint>
@@ -117,13 +118,25 @@ size_t morton_temp_bytes(int64_t m, int dim) {
     return bytes;
 }
 
-int morton_order(const float* d_queries, int64_t m, int dim, const MortonFrame& f,
+int morton_order(const float* d_queries, int64_t m, int dim, const MortonFrame& frame,
                  uint32_t* keys_in, uint32_t* keys_out, uint32_t* ids_in, uint32_t* ids_out,
                  void* temp, size_t temp_bytes, cudaStream_t st) {
     const unsigned grid = unsigned((m + 255) / 256);
+    // Resolution follows the batch: about 1.7 cells per query (C3, clustered:
+    // 10M queries -> 8 bits per axis, a 1.25M host-path chunk -> 7, where 8
+    // costs 0.092 vs 0.055 ms of ordering for the same walk time).
+    MortonFrame f = frame;
+    if (dim >= 1 && dim <= 8 && m > 0) {
+        const int fit = int(std::floor(std::log2(double(m) * 1.7) / dim));
+        const int b = std::max(1, std::min(frame.bits, fit));
+        if (b < frame.bits) {
+            const float ratio = float((1u << b) - 1u) / float((1u << frame.bits) - 1u);
+            for (int d = 0; d < dim; ++d) f.scale[d] = frame.scale[d] * ratio;
+            f.bits = b;
+        }
+    }
     if (use_counting(m, dim)) {
-        const int64_t bins = key_bins(dim);
-        if (bins != (int64_t(1) << (f.bits * dim))) return -1;
+        const int64_t bins = int64_t(1) << (f.bits * dim);  // <= key_bins(dim), which sized temp
         uint32_t* cnt = static_cast<uint32_t*>(temp);
         uint32_t* offs = reinterpret_cast<uint32_t*>(static_cast<char*>(temp) + align_up(size_t(bins) * 4));
         void* stmp = static_cast<char*>(temp) + 2 * align_up(size_t(bins) * 4);
