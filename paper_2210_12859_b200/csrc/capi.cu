@@ -911,7 +911,7 @@ fkd_status fkd_run_batch(const fkd_tree* t, const float* queries, int64_t m, int
     // c mod R's buffers after chunk c-R's walk / D2H.
     std::vector<char> full(ndev, 0);
     if (err == FKD_OK) {
-        static const int full_env = [] {  // experiment knob: FKD_FULL_STAGING=0 forces the ring
+        const int full_env = [] {  // experiment knob: FKD_FULL_STAGING=0 forces the ring
             const char* e = std::getenv("FKD_FULL_STAGING");
             return e ? std::atoi(e) : 1;
         }();

@@ -433,3 +433,39 @@ def test_concurrent_callers_share_one_tree(oracle):
     for th in threads:
         th.join()
     assert not errors, errors
+
+
+@pytest.mark.parametrize("staging,streams,chunk_div,budget,first_div", [
+    ("1", "4", "8", "-1", "1"),     # defaults: full staging, graduated chunks
+    ("0", "4", "8", "-1", "1"),     # ring staging (slot reuse waits)
+    ("1", "2", "16", "40", "4"),    # forced overflow in every chunk, smaller first budget
+    ("0", "3", "5", "7", "1"),      # ring + forced overflow + resume
+])
+def test_host_pipeline_chunks_exact(oracle, staging, streams, chunk_div, budget, first_div, monkeypatch):
+    """fkd_run_batch's chunked pipeline (capi.cu: copy-in stream, slot streams,
+    high-priority tail stream, copy-out stream; full or ring staging) returns
+    exactly the oracle's results and the device path's, with over-budget
+    queries finished inside the chunks."""
+    import torch
+    monkeypatch.setenv("FKD_FULL_STAGING", staging)
+    monkeypatch.setenv("FKD_STREAMS", streams)
+    monkeypatch.setenv("FKD_CHUNK_DIV", chunk_div)
+    monkeypatch.setenv("FKD_BUDGET", budget)
+    monkeypatch.setenv("FKD_FIRST_BUDGET_DIV", first_div)
+    monkeypatch.setenv("FKD_RESUME_MIN", "50")
+    pts = fk.clustered_points(5, 1, 60_000, 3)
+    qs = fk.clustered_points(5, 2, 2_600_001, 3)[::5].copy()  # 520,001 queries: several 256k-capped chunks
+    nodes = oracle.build_tree(pts)
+    tree = fk.KdTree.from_level_order(nodes)
+    for kind, k, r in ((fk.QueryKind.fcp, 1, INF), (fk.QueryKind.knn, 8, INF), (fk.QueryKind.knn, 20, 0.01)):
+        res = fk.run_batch(tree, qs, fk.BatchOptions(kind=kind, k=k, max_radius=r))
+        sample = np.arange(0, len(qs), 97)
+        ref = oracle.run_batch(nodes, qs[sample], "knn" if kind == fk.QueryKind.knn else "fcp", k, r)
+        assert np.array_equal(res.counts[sample], ref[0])
+        assert res.hits.reshape(len(qs), -1)[sample].tobytes() == ref[1].reshape(len(sample), -1).tobytes()
+        dq = torch.from_numpy(qs).cuda()
+        c = torch.empty(len(qs), dtype=torch.int32, device="cuda")
+        h = torch.empty(len(qs) * k, dtype=torch.int64, device="cuda")
+        fk.run_batch_device(tree, dq, c, h, fk.BatchOptions(kind=kind, k=k, max_radius=r))
+        assert np.array_equal(c.cpu().numpy(), res.counts)
+        assert h.cpu().numpy().tobytes() == res.hits.tobytes()
