@@ -921,12 +921,15 @@ fkd_status fkd_run_batch(const fkd_tree* t, const float* queries, int64_t m, int
             int64_t shard = 0;
             for (const Job& j : jobs)
                 if (j.rep == di) shard += j.count;
-            size_t free_b = 0, total_b = 0;
-            cudaMemGetInfo(&free_b, &total_b);
             Workspace* w0 = wss[di][0];
             const int64_t have = std::min({w0->q_cap / std::max(1, dim), w0->c_cap, w0->h_cap / k});
-            const double need = double(shard) * (double(dim) * 4 + 4 + 8.0 * k);
-            full[di] = full_env != 0 && (have >= shard || need <= 0.25 * double(free_b));
+            bool fits = have >= shard;
+            if (!fits && full_env != 0) {
+                size_t free_b = 0, total_b = 0;
+                cudaMemGetInfo(&free_b, &total_b);
+                fits = double(shard) * (double(dim) * 4 + 4 + 8.0 * k) <= 0.25 * double(free_b);
+            }
+            full[di] = full_env != 0 && fits;
             for (Workspace* w : wss[di]) {
                 int64_t big = 0;
                 for (const Job& j : jobs)

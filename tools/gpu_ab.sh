@@ -1,7 +1,4 @@
-python tools/quickbench.py --sorted-only --clustered --m 1250000 --configs fcp,knn8 --reps 5 2>&1 | grep true
-python tools/quickbench.py --sorted-only --clustered --m 312500 --configs fcp,knn8 --reps 5 2>&1 | grep true
-python tools/quickbench.py --sorted-only --clustered --configs fcp,knn8 --reps 3 2>&1 | grep true
-python tools/quickbench.py --sorted-only --configs fcp,knn8 --reps 3 2>&1 | grep true
-python tools/quickbench.py --sorted-only --dim 4 --m 2000000 --configs fcp,knn8 --reps 3 2>&1 | grep true
+for v in "1 1" "0 1" "1 0" "0 0"; do set -- $v; echo "full $1 prio $2"; export FKD_FULL_STAGING=$1 FKD_TAIL_PRIO=$2
 python tools/e2e_diag.py 2>&1 | grep auto
-python -m pytest tests -m gpu -x -q 2>&1 | tail -1
+python bench.py --steps 10 --warmup 3 --no-cpu-baseline 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('bench', d['value']/1e6, d['e2e']['value']/1e6)"
+done
