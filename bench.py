@@ -346,7 +346,9 @@ def run_b200(args) -> None:
         hc, hh = host_out[(kind, k)]
         c, h = outs[(kind, k)]
         got_c = np.ctypeslib.as_array(C.cast(hc, C.POINTER(C.c_int32)), shape=(m,))
+        got_h = np.ctypeslib.as_array(C.cast(hh, C.POINTER(C.c_int64)), shape=(m * k,))
         e2e_parity &= bool(np.array_equal(got_c, c.cpu().numpy()))
+        e2e_parity &= bool(np.array_equal(got_h, h.view(torch.int64).cpu().numpy()))
     for hc, hh in host_out.values():
         fk.LIB.fkd_host_free(hc)
         fk.LIB.fkd_host_free(hh)
