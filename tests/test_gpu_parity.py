@@ -469,3 +469,43 @@ def test_host_pipeline_chunks_exact(oracle, staging, streams, chunk_div, budget,
         fk.run_batch_device(tree, dq, c, h, fk.BatchOptions(kind=kind, k=k, max_radius=r))
         assert np.array_equal(c.cpu().numpy(), res.counts)
         assert h.cpu().numpy().tobytes() == res.hits.tobytes()
+
+
+@pytest.mark.parametrize("mode", ["pageable-staged", "pageable-direct", "pinned"])
+def test_host_buffers_pinned_and_pageable(oracle, mode, monkeypatch):
+    """fkd_run_batch with pinned caller buffers, with pageable ones staged
+    through the library's pinned pool (CopyPool, capi.cu), and with pageable
+    ones handed to cudaMemcpyAsync directly (FKD_PAGEABLE_STAGING=0): the
+    same bytes as the device path in every mode."""
+    import ctypes as C
+    import torch
+    monkeypatch.setenv("FKD_PAGEABLE_STAGING", "0" if mode == "pageable-direct" else "1")
+    pts = fk.clustered_points(6, 1, 50_000, 3)
+    qs = fk.clustered_points(6, 2, 700_001, 3)
+    tree = fk.KdTree.from_level_order(oracle.build_tree(pts))
+    m = len(qs)
+    for kind, k in ((fk.QueryKind.fcp, 1), (fk.QueryKind.knn, 8)):
+        o = fk.BatchOptions(kind=kind, k=k).to_c()
+        if mode == "pinned":
+            hq = fk.LIB.fkd_host_alloc(qs.nbytes)
+            C.memmove(hq, qs.ctypes.data, qs.nbytes)
+            hc, hh = fk.LIB.fkd_host_alloc(m * 4), fk.LIB.fkd_host_alloc(m * k * 8)
+            qa, ca, ha = hq, hc, hh
+        else:
+            counts = np.full(m, -7, np.int32)
+            hits = np.full(m * k, -7, np.int64)
+            qa, ca, ha = qs.ctypes.data, counts.ctypes.data, hits.ctypes.data
+        rc = fk.LIB.fkd_run_batch(tree.handle, C.c_void_p(qa), m, 3, C.byref(o), C.c_void_p(ca),
+                                  C.c_void_p(ha), None)
+        assert rc == 0, fk.LIB.fkd_last_error()
+        got_c = np.ctypeslib.as_array(C.cast(C.c_void_p(ca), C.POINTER(C.c_int32)), shape=(m,)).copy()
+        got_h = np.ctypeslib.as_array(C.cast(C.c_void_p(ha), C.POINTER(C.c_int64)), shape=(m * k,)).copy()
+        if mode == "pinned":
+            for p in (hq, hc, hh):
+                fk.LIB.fkd_host_free(p)
+        dq = torch.from_numpy(qs).cuda()
+        c = torch.empty(m, dtype=torch.int32, device="cuda")
+        h = torch.empty(m * k, dtype=torch.int64, device="cuda")
+        fk.run_batch_device(tree, dq, c, h, fk.BatchOptions(kind=kind, k=k))
+        assert np.array_equal(got_c, c.cpu().numpy())
+        assert np.array_equal(got_h, h.cpu().numpy())
