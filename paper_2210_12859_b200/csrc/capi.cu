@@ -45,15 +45,42 @@ fkd_status fail(fkd_status s, const std::string& msg) {
 constexpr int64_t kSortChunk = int64_t(1) << 30;  // u32 ids, int item counts in CUB
 
 struct Tuning {
-    int budget = -1;  // -1: per kind (measured on C3: fcp 1024, kNN 3072 loop trips)
+    int budget = -1;  // -1: per kind (first_budget: fcp 112, kNN 256 loop trips, then the rounds)
     int wave = 0;
     std::vector<int> rounds{64, 64, 128, 256, 512, 1024};
     int64_t resume_min = 0;  // 0: SMs x 64 (measured: 8-D and 4-D kNN64 tails; C3's ~2k stay on the CTA pass)
     int resume_trips = 0;    // 0: 4 x budget (measured: 8-D fcp 4096, kNN8/16 12288 best); <0: unbounded
+    // continuation rounds after the budgeted walk (walk_round_kernel), trips
+    // per round.  Measured (tools/rounds_ab.sh, profiles/r01e_rounds_*): fcp
+    // walk -14% (3-D C3) to -30% (4-D), kNN4 4-D -18%; for lists of >= 8
+    // slots parking costs what the denser warps save (C3 kNN8 walk + tail
+    // 9.06 vs 9.03 ms, 4-D kNN20 +48%), so those keep one long budgeted walk.
+    std::vector<int> rounds_fcp{112, 224, 448}, rounds_knn{256, 512};
+    bool rounds_knn_all = false;  // FKD_RROUNDS_KNN given: every kNN bucket
 };
 
+int walk_bucket_of(int k);
+// the rounds run for register lists of <= 4 slots (fcp, k <= 4)
+inline bool rounds_on(int k) { return walk_bucket_of(k) <= 4; }
+// first walk's loop trips before a query parks (FKD_BUDGET < 0: per kind)
+inline int first_budget(int k) { return k == 1 ? 112 : (rounds_on(k) ? 256 : 3072); }
+// resume pass trips (FKD_RESUME_TRIPS = 0): 4 x the per-kind budget without rounds
+inline int resume_trips_default(int k) { return 4 * (k == 1 ? 1024 : 3072); }
+
+std::vector<int> parse_ints(const char* e) {
+    std::vector<int> v;
+    for (const char* p = e; *p;) {
+        const int x = std::atoi(p);
+        if (x > 0) v.push_back(x);
+        while (*p && *p != ',') ++p;
+        if (*p == ',') ++p;
+    }
+    return v;
+}
+
 // Launch tuning, overridable per call for experiments and tests:
-// FKD_BUDGET=<loop trips before the overflow pass; <0 per kind, 0 off>,
+// FKD_BUDGET=<first walk's loop trips before a query parks; <0 per kind, 0 off>,
+// FKD_RROUNDS_FCP / FKD_RROUNDS_KNN=<t1,t2,..> (continuation rounds; "0": none),
 // FKD_RESUME_MIN=<overflow count that selects the resume pass>,
 // FKD_RESUME_TRIPS=<steps the resume pass adds before the CTA pass; <0 unbounded>,
 // FKD_WAVE=1 + FKD_ROUNDS=<t1,t2,..> (wave rounds, off: measured slower).
@@ -64,6 +91,11 @@ Tuning tuning() {
         if (const char* e = std::getenv("FKD_WAVE")) x.wave = std::atoi(e) != 0;
         if (const char* e = std::getenv("FKD_RESUME_MIN")) x.resume_min = std::atoll(e);
         if (const char* e = std::getenv("FKD_RESUME_TRIPS")) x.resume_trips = std::atoi(e);
+        if (const char* e = std::getenv("FKD_RROUNDS_FCP")) x.rounds_fcp = parse_ints(e);
+        if (const char* e = std::getenv("FKD_RROUNDS_KNN")) {
+            x.rounds_knn = parse_ints(e);
+            x.rounds_knn_all = true;
+        }
         if (const char* e = std::getenv("FKD_ROUNDS")) {  // e.g. "64,64,128"
             x.rounds.clear();
             for (const char* p = e; *p;) {
@@ -467,7 +499,7 @@ fkd_status enqueue(const fkd_tree* t, Replica& r, Workspace* w, const float* d_q
         a.bad = w->small;
         a.id_base = id_offset + base;
         const Tuning tu = tuning();
-        int budget = tu.budget >= 0 ? tu.budget : (k == 1 ? 1024 : 3072);
+        int budget = tu.budget >= 0 ? tu.budget : first_budget(k);
         if (budget_div > 1 && budget > 0) budget = std::max(64, budget / budget_div);
         a.budget = (stats || walk_bucket_of(k) == 0 || t->dim > 8) ? 0 : budget;
         if (a.budget > 0) {
@@ -535,6 +567,32 @@ fkd_status enqueue(const fkd_tree* t, Replica& r, Workspace* w, const float* d_q
                 FKD_CUDA(cudaStreamWaitEvent(tail_st, w->pe[3], 0));
             }
             const cudaStream_t ts = (a.budget > 0 && tail_st) ? tail_st : st;
+            static const std::vector<int> none;
+            const std::vector<int>& rounds =
+                k == 1 ? tu.rounds_fcp : ((rounds_on(k) || tu.rounds_knn_all) ? tu.rounds_knn : none);
+            if (a.budget > 0 && !rounds.empty()) {
+                // continuation rounds: the parked walks, compacted into dense
+                // warps, continue for `trips` more trips per round; lists
+                // ping-pong between ovf_ids and the upper half of wave_ids
+                const int64_t half = w->wave_cap / 2;
+                uint32_t* lists[2] = {a.ovf_ids, w->wave_ids + half};
+                unsigned long long* cnts[2] = {a.ovf_count, w->small + 10};
+                int cur = 0;
+                for (int trips : rounds) {
+                    WalkArgs r = a;
+                    r.trips = trips;
+                    r.wave_in = lists[cur];
+                    r.wave_n_in = cnts[cur];
+                    r.wave_out = lists[cur ^ 1];
+                    r.wave_n_out = cnts[cur ^ 1];
+                    FKD_CUDA(cudaMemsetAsync(cnts[cur ^ 1], 0, sizeof(unsigned long long), ts));
+                    nl += launch_walk(r, t->dim, t->stride, stats, unordered, 3, ts);
+                    FKD_CUDA(cudaGetLastError());
+                    cur ^= 1;
+                }
+                a.ovf_ids = lists[cur];
+                a.ovf_count = cnts[cur];
+            }
             if (a.budget > 0) {
                 // resume pass: continues the parked walks with the plain grid
                 // when at least resume_min overflowed (decided on the device)
@@ -544,7 +602,8 @@ fkd_status enqueue(const fkd_tree* t, Replica& r, Workspace* w, const float* d_q
                 a.wave_out = w->wave_ids;
                 a.wave_n_out = w->small + 8;
                 WalkArgs r = a;
-                r.trips = tu.resume_trips > 0 ? tu.resume_trips : (tu.resume_trips < 0 ? 0x7fffffff : 4 * a.budget);
+                r.trips = tu.resume_trips > 0 ? tu.resume_trips
+                                              : (tu.resume_trips < 0 ? 0x7fffffff : resume_trips_default(k));
                 r.wave_in = a.ovf_ids;
                 r.wave_n_in = a.ovf_count;
                 nl += launch_walk(r, t->dim, t->stride, stats, unordered, 2, ts);

@@ -223,6 +223,7 @@ struct LaneWalk {
     // split dimension: qr holds the query rotated so that qr[0] is the
     // coordinate split at the current depth (rotated by one per level).
     static constexpr bool kRot = S > D && D > 1;
+    static constexpr int kKB = KB;
     float q[D];
     float qr[kRot ? D : 1];
     uint64_t L[KB];
@@ -393,8 +394,20 @@ struct LaneWalk {
         prev = st.y;
         d = depth_of(curr) % D;
         if constexpr (kRot) {
+            // qr[j] = q[(d + j) % D] as d predicated one-place rotations: a
+            // select chain on d is folded back into a dynamic index by the
+            // compiler, which puts the whole walk state in local memory
 #pragma unroll
-            for (int j = 0; j < D; ++j) qr[j] = q[(d + j) % D];
+            for (int j = 0; j < D; ++j) qr[j] = q[j];
+#pragma unroll
+            for (int r = 0; r < D - 1; ++r) {
+                const bool more = r < d;
+                float t[D];
+#pragma unroll
+                for (int j = 0; j < D; ++j) t[j] = more ? qr[(j + 1) % D] : qr[j];
+#pragma unroll
+                for (int j = 0; j < D; ++j) qr[j] = t[j];
+            }
         }
         cnt = Counters<STATS>();
     }
@@ -474,6 +487,28 @@ constexpr int walk_min_blocks() {
     return KB == 8 ? FKD_MINB_KB8 : (KB == 16 ? FKD_MINB_KB16 : 1);
 }
 
+// Walks until the root exits (false) or about `trips` loop trips have run
+// (true: the walk is parked at (curr, prev)).  Several steps per budget
+// check (measured on C3: fcp 8 steps, -7% then -3% vs 1; kNN 4 steps, 8 is
+// +1.5%); the budget is approximate by a few trips, which nothing depends on.
+template <class W>
+__device__ __forceinline__ bool walk_budgeted(W& w, const WalkArgs& a, int trips) {
+    constexpr int kSteps = W::kKB == 1 ? 8 : 4;
+    while (true) {
+        if (!w.step(a)) return false;
+        if (!w.step(a)) return false;
+        if (!w.step(a)) return false;
+        if (!w.step(a)) return false;
+        if constexpr (kSteps == 8) {
+            if (!w.step(a)) return false;
+            if (!w.step(a)) return false;
+            if (!w.step(a)) return false;
+            if (!w.step(a)) return false;
+        }
+        if ((trips -= kSteps) <= 0) return true;
+    }
+}
+
 // One thread per walk position (plain grid).
 template <int D, int S, int KB, bool STATS, bool UNORDERED>
 __global__ void __launch_bounds__(kWalkThreads, walk_min_blocks<KB>()) walk_kernel(const WalkArgs a) {
@@ -490,24 +525,7 @@ __global__ void __launch_bounds__(kWalkThreads, walk_min_blocks<KB>()) walk_kern
                 // several steps per budget check (measured on C3: fcp 8 steps,
                 // -7% then -3% vs 1; kNN 4 steps, 8 is +1.5%); the budget is
                 // approximate by a few trips, which nothing depends on
-                constexpr int kSteps = KB == 1 ? 8 : 4;
-                int trips = a.budget;
-                while (true) {
-                    if (!w.step(a)) break;
-                    if (!w.step(a)) break;
-                    if (!w.step(a)) break;
-                    if (!w.step(a)) break;
-                    if constexpr (kSteps == 8) {
-                        if (!w.step(a)) break;
-                        if (!w.step(a)) break;
-                        if (!w.step(a)) break;
-                        if (!w.step(a)) break;
-                    }
-                    if ((trips -= kSteps) <= 0) {
-                        over = true;
-                        break;
-                    }
-                }
+                over = walk_budgeted(w, a, a.budget);
             }
         }
         w.finish(a);  // over budget: the partial list stays as the overflow pass's bound
@@ -518,6 +536,41 @@ __global__ void __launch_bounds__(kWalkThreads, walk_min_blocks<KB>()) walk_kern
     }
     if (active) add_totals<STATS>(a, w.cnt.steps, w.cnt.visited, w.cnt.processed);
     else add_totals<STATS>(a, 0, 0, 0);
+}
+
+// Continuation round (compaction rounds): one thread per id
+// of the previous round's parked list, which is dense again, so a warp's 32
+// lanes are 32 live walks instead of the few stragglers of a warp of the
+// walk kernel.  Each resumes its (curr, prev) + partial list, walks at most
+// `trips` more trips, and either finishes or parks again onto the next list
+// (warp-aggregated append in lane order, so Morton neighbours stay
+// together).  The grid is sized for the largest possible list; blocks past
+// the device-side count exit at once.
+template <int D, int S, int KB, bool UNORDERED>
+__global__ void __launch_bounds__(kWalkThreads, walk_min_blocks<KB>()) walk_round_kernel(const WalkArgs a) {
+    const int64_t items = int64_t(*a.wave_n_in);
+    const int64_t first = int64_t(blockIdx.x) * blockDim.x;
+    if (first >= items) return;
+    const int64_t i = first + threadIdx.x;
+    bool park = false;
+    uint32_t qid = 0;
+    if (i < items) {  // the walk state lives only inside this block (kept in registers)
+        LaneWalk<D, S, KB, false, UNORDERED> w;
+        qid = a.wave_in[i];
+        w.resume(a, int32_t(qid));
+        park = walk_budgeted(w, a, a.trips);
+        w.finish(a);
+        if (park) a.wave_state[qid] = make_int2(w.curr, w.prev);
+    }
+    const unsigned lane = threadIdx.x & 31u;
+    const unsigned mask = __ballot_sync(0xffffffffu, park);
+    if (mask) {
+        const unsigned leader = __ffs(mask) - 1;
+        unsigned long long base = 0;
+        if (lane == leader) base = atomicAdd(a.wave_n_out, (unsigned long long)__popc(mask));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        if (park) a.wave_out[base + __popc(mask & ((1u << lane) - 1u))] = qid;
+    }
 }
 
 // Wave round: every live query walks at most `trips` loop trips; walks that

@@ -53,13 +53,25 @@ void launch_wave(const WalkArgs& a, cudaStream_t st) {
     kern<<<grid, 256, 0, st>>>(a);
 }
 
+template <int D, int S, int KB, bool UNORDERED>
+void launch_round(const WalkArgs& a, cudaStream_t st) {
+    walk_round_kernel<D, S, KB, UNORDERED><<<walk_blocks(a.m, kWalkThreads), kWalkThreads, 0, st>>>(a);
+}
+
 // phase 0: the walk kernel; phase 1: the overflow pass (when budgeted);
-// phase 2: one wave round.
+// phase 2: one wave round (resume pass); phase 3: one continuation round.
 template <int D, int S, int KB>
 int launch_bucket(const WalkArgs& a, bool stats, bool unordered, int phase, cudaStream_t st) {
     if (phase == 1) {
         if (stats || a.budget <= 0) return 0;
         launch_overflow<D, S, KB>(a, st);
+        return 1;
+    }
+    if (phase == 3) {
+        if (unordered)
+            launch_round<D, S, KB, true>(a, st);
+        else
+            launch_round<D, S, KB, false>(a, st);
         return 1;
     }
     if (phase == 2) {

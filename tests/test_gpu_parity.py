@@ -196,19 +196,27 @@ def test_cpp_shim_against_reference():
     assert "OK" in out.stdout
 
 
-@pytest.mark.parametrize("budget,resume_min,resume_trips", [
-    ("1", "0", "0"), ("3", "0", "0"), ("50", "0", "0"),   # CTA pass only (few overflow)
-    ("2", "1", "-1"), ("40", "1", "-1"),                   # unbounded resume pass
-    ("2", "1", "3"), ("5", "1", "40"), ("40", "1", "0"),   # budgeted resume, survivors -> CTA pass
+@pytest.mark.parametrize("budget,resume_min,resume_trips,rounds", [
+    ("1", "0", "0", "0"), ("3", "0", "0", "0"), ("50", "0", "0", "0"),   # CTA pass only (few overflow)
+    ("2", "1", "-1", "0"), ("40", "1", "-1", "0"),                       # unbounded resume pass
+    ("2", "1", "3", "0"), ("5", "1", "40", "0"), ("40", "1", "0", "0"),  # budgeted resume, survivors -> CTA pass
+    ("1", "0", "0", "1,1,2,3"), ("4", "0", "0", "4,8"),                  # continuation rounds -> CTA pass
+    ("2", "1", "6", "1,2,4"), ("8", "1", "-1", "8"),                     # rounds -> resume pass -> CTA pass
+    ("-1", "0", "0", "-"),                                               # the defaults
 ])
-def test_overflow_pass_is_exact(oracle, budget, resume_min, resume_trips, monkeypatch):
-    """Queries stopped by the walk budget are finished by the CTA-per-query
-    overflow pass (overflow.cuh) or, when many overflow (FKD_RESUME_MIN=1
-    forces it), resumed from their parked (curr, prev) by the plain-grid resume
-    pass for FKD_RESUME_TRIPS more steps, whose survivors are parked again and
-    handed to the CTA pass; results must stay bit-exact in every combination."""
+def test_overflow_pass_is_exact(oracle, budget, resume_min, resume_trips, rounds, monkeypatch):
+    """Queries stopped by the walk budget continue in compacted continuation
+    rounds (walk_round_kernel, FKD_RROUNDS_*), then are finished by the
+    CTA-per-query overflow pass (overflow.cuh) or, when many remain
+    (FKD_RESUME_MIN=1 forces it), resumed from their parked (curr, prev) by the
+    plain-grid resume pass for FKD_RESUME_TRIPS more steps, whose survivors are
+    parked again and handed to the CTA pass; results must stay bit-exact in
+    every combination."""
     monkeypatch.setenv("FKD_BUDGET", budget)
     monkeypatch.setenv("FKD_RESUME_TRIPS", resume_trips)
+    if rounds != "-":
+        monkeypatch.setenv("FKD_RROUNDS_FCP", rounds)
+        monkeypatch.setenv("FKD_RROUNDS_KNN", rounds)
     if resume_min != "0":
         monkeypatch.setenv("FKD_RESUME_MIN", resume_min)
     else:
