@@ -394,8 +394,8 @@ def run_b200(args) -> None:
                 "d2h_bytes_per_step": d2h, "results_equal_device_path": bool(e2e_parity),
                 "path": "fkd_run_batch (C ABI, pinned host buffers, chunked H2D/walk/D2H)"},
         "gpu_launches": launches // args.steps,
-        "gpu_launches_note": "own kernels per timed step (per batch: Morton keys, walk, resume pass, "
-                             "overflow pass); CUB sort kernels excluded",
+        "gpu_launches_note": "own kernels per timed step (per batch: Morton keys, walk, continuation "
+                             "rounds (fcp: 3), resume pass, CTA overflow pass); CUB sort kernels excluded",
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": f"walk {kind}{'' if kind == 'fcp' else k} (dominant)",
