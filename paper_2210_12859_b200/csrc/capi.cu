@@ -45,11 +45,9 @@ fkd_status fail(fkd_status s, const std::string& msg) {
 constexpr int64_t kSortChunk = int64_t(1) << 30;  // u32 ids, int item counts in CUB
 
 struct Tuning {
-    int budget = -1;  // -1: per kind (first_budget: fcp 112, kNN 256 loop trips, then the rounds)
-    int wave = 0;
-    std::vector<int> rounds{64, 64, 128, 256, 512, 1024};
+    int budget = -1;  // -1: per kind (first_budget: fcp 112, kNN <= 4 slots 256, larger lists 3072 loop trips)
     int64_t resume_min = 0;  // 0: SMs x 64 (measured: 8-D and 4-D kNN64 tails; C3's ~2k stay on the CTA pass)
-    int resume_trips = 0;    // 0: 4 x budget (measured: 8-D fcp 4096, kNN8/16 12288 best); <0: unbounded
+    int resume_trips = 0;    // 0: fcp 4096, kNN 12288 (measured on 8-D); <0: unbounded
     // continuation rounds after the budgeted walk (walk_round_kernel), trips
     // per round.  Measured (tools/rounds_ab.sh, profiles/r01e_rounds_*): fcp
     // walk -14% (3-D C3) to -30% (4-D), kNN4 4-D -18%; for lists of >= 8
@@ -83,28 +81,16 @@ std::vector<int> parse_ints(const char* e) {
 // FKD_RROUNDS_FCP / FKD_RROUNDS_KNN=<t1,t2,..> (continuation rounds; "0": none),
 // FKD_RESUME_MIN=<overflow count that selects the resume pass>,
 // FKD_RESUME_TRIPS=<steps the resume pass adds before the CTA pass; <0 unbounded>,
-// FKD_WAVE=1 + FKD_ROUNDS=<t1,t2,..> (wave rounds, off: measured slower).
 Tuning tuning() {
     return [] {
         Tuning x;
         if (const char* e = std::getenv("FKD_BUDGET")) x.budget = std::atoi(e);  // <0: per kind, 0: off
-        if (const char* e = std::getenv("FKD_WAVE")) x.wave = std::atoi(e) != 0;
         if (const char* e = std::getenv("FKD_RESUME_MIN")) x.resume_min = std::atoll(e);
         if (const char* e = std::getenv("FKD_RESUME_TRIPS")) x.resume_trips = std::atoi(e);
         if (const char* e = std::getenv("FKD_RROUNDS_FCP")) x.rounds_fcp = parse_ints(e);
         if (const char* e = std::getenv("FKD_RROUNDS_KNN")) {
             x.rounds_knn = parse_ints(e);
             x.rounds_knn_all = true;
-        }
-        if (const char* e = std::getenv("FKD_ROUNDS")) {  // e.g. "64,64,128"
-            x.rounds.clear();
-            for (const char* p = e; *p;) {
-                const int v = std::atoi(p);
-                if (v > 0) x.rounds.push_back(v);
-                while (*p && *p != ',') ++p;
-                if (*p == ',') ++p;
-            }
-            if (x.rounds.empty()) x.wave = 0;
         }
         return x;
     }();
@@ -144,7 +130,7 @@ struct Workspace {
     unsigned long long* small = nullptr;    // [8]: bad, steps, visited, processed, work, ovf count, ovf next
     uint32_t* ovf = nullptr;                // overflow query ids
     int64_t ovf_cap = 0;
-    uint32_t* wave_ids = nullptr;           // [2 * cap] wave id lists
+    uint32_t* wave_ids = nullptr;           // [2 * cap] parked-id lists (rounds, resume pass)
     int64_t wave_cap = 0;
     int2* wave_state = nullptr;             // [cap]
     int64_t wave_state_cap = 0;
@@ -528,34 +514,7 @@ fkd_status enqueue(const fkd_tree* t, Replica& r, Workspace* w, const float* d_q
         if (ev_mid && base == 0) FKD_CUDA(cudaEventRecord(ev_mid, st));
         const bool unordered = (o->flags & FKD_FLAG_UNORDERED) != 0;
         int nl = 0;
-        const bool wave = tu.wave && a.budget > 0;
-        if (wave) {
-            // wave rounds (walk.cuh walk_wave_kernel); survivors of the last
-            // round feed the overflow pass through the same id list
-            FKD_CUDA(grow(w->wave_ids, w->wave_cap, 2 * cm));
-            FKD_CUDA(grow(w->wave_state, w->wave_state_cap, cm));
-            const int64_t half = w->wave_cap / 2;
-            a.wave_state = w->wave_state;
-            a.wave_in = nullptr;
-            a.wave_n_in = nullptr;
-            int r = 0;
-            for (int trips : tu.rounds) {
-                a.trips = trips;
-                a.wave_out = w->wave_ids + (r & 1) * half;
-                a.wave_n_out = w->small + 8 + (r & 1);
-                FKD_CUDA(cudaMemsetAsync(a.wave_n_out, 0, sizeof(unsigned long long), st));
-                const int l = launch_walk(a, t->dim, t->stride, stats, unordered, 2, st);
-                if (l <= 0) return fail(FKD_CUDA_ERROR, "no wave kernel for this configuration");
-                FKD_CUDA(cudaGetLastError());
-                nl += l;
-                a.wave_in = a.wave_out;
-                a.wave_n_in = a.wave_n_out;
-                ++r;
-            }
-            a.ovf_ids = const_cast<uint32_t*>(a.wave_in);
-            a.ovf_count = const_cast<unsigned long long*>(a.wave_n_in);
-            a.resume_min = 0;  // the overflow pass takes every survivor
-        } else {
+        {
             nl = launch_walk(a, t->dim, t->stride, stats, unordered, 0, st);
             if (nl <= 0) return fail(FKD_CUDA_ERROR, "no kernel for this configuration");
             FKD_CUDA(cudaGetLastError());
@@ -581,6 +540,7 @@ fkd_status enqueue(const fkd_tree* t, Replica& r, Workspace* w, const float* d_q
                 for (int trips : rounds) {
                     WalkArgs r = a;
                     r.trips = trips;
+                    r.resume_min = 0;  // every round runs, whatever the count
                     r.wave_in = lists[cur];
                     r.wave_n_in = cnts[cur];
                     r.wave_out = lists[cur ^ 1];
@@ -594,10 +554,11 @@ fkd_status enqueue(const fkd_tree* t, Replica& r, Workspace* w, const float* d_q
                 a.ovf_count = cnts[cur];
             }
             if (a.budget > 0) {
-                // resume pass: continues the parked walks with the plain grid
-                // when at least resume_min overflowed (decided on the device)
-                // for at most resume_trips more steps; its survivors (parked
-                // again) are the CTA pass's list
+                // resume pass: one more round (walk_round_kernel), run only
+                // when at least resume_min walks are still parked (decided on
+                // the device: bulk long walks, e.g. 8-D), for at most
+                // resume_trips more steps; its survivors (parked again) are the
+                // CTA pass's list
                 FKD_CUDA(cudaMemsetAsync(w->small + 8, 0, sizeof(unsigned long long), ts));
                 a.wave_out = w->wave_ids;
                 a.wave_n_out = w->small + 8;
@@ -606,11 +567,11 @@ fkd_status enqueue(const fkd_tree* t, Replica& r, Workspace* w, const float* d_q
                                               : (tu.resume_trips < 0 ? 0x7fffffff : resume_trips_default(k));
                 r.wave_in = a.ovf_ids;
                 r.wave_n_in = a.ovf_count;
-                nl += launch_walk(r, t->dim, t->stride, stats, unordered, 2, ts);
+                nl += launch_walk(r, t->dim, t->stride, stats, unordered, 3, ts);
                 FKD_CUDA(cudaGetLastError());
             }
         }
-        const cudaStream_t ts = (a.budget > 0 && tail_st && !wave) ? tail_st : st;
+        const cudaStream_t ts = (a.budget > 0 && tail_st) ? tail_st : st;
         if (ev_tail && base == 0) FKD_CUDA(cudaEventRecord(ev_tail, ts));
         const int tail = launch_walk(a, t->dim, t->stride, stats, unordered, 1, ts);  // overflow pass
         FKD_CUDA(cudaGetLastError());

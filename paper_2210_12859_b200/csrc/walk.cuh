@@ -61,9 +61,9 @@ struct WalkArgs {
     uint32_t* ovf_ids;          // [m] ids of queries over budget
     unsigned long long* ovf_count;
     unsigned long long* ovf_next;
-    // wave rounds (walk_wave_kernel)
+    // continuation rounds / resume pass (walk_round_kernel)
     int32_t trips;                         // loop trips per query this round
-    const uint32_t* wave_in;               // ids walked this round (null: all walk positions)
+    const uint32_t* wave_in;               // ids walked this round
     const unsigned long long* wave_n_in;   // their count (device)
     uint32_t* wave_out;                    // ids still walking after this round
     unsigned long long* wave_n_out;
@@ -367,7 +367,7 @@ struct LaneWalk {
         return true;
     }
 
-    // Resumes a walk suspended by an earlier wave round: the state is the
+    // Resumes a walk parked by an earlier pass (walk budget or round): the state is the
     // reference's two node ids; the candidate list is the partial one the
     // round left in the query's own output slot; radius2 and the split
     // dimension are recomputed from them.
@@ -546,9 +546,13 @@ __global__ void __launch_bounds__(kWalkThreads, walk_min_blocks<KB>()) walk_kern
 // (warp-aggregated append in lane order, so Morton neighbours stay
 // together).  The grid is sized for the largest possible list; blocks past
 // the device-side count exit at once.
+// The same kernel is the resume pass: with resume_min > 0 it runs only when
+// at least that many walks are parked (bulk long walks, e.g. 8-D), else the
+// CTA pass takes them all (overflow.cuh reads the same count).
 template <int D, int S, int KB, bool UNORDERED>
 __global__ void __launch_bounds__(kWalkThreads, walk_min_blocks<KB>()) walk_round_kernel(const WalkArgs a) {
     const int64_t items = int64_t(*a.wave_n_in);
+    if (a.resume_min > 0 && items < a.resume_min) return;
     const int64_t first = int64_t(blockIdx.x) * blockDim.x;
     if (first >= items) return;
     const int64_t i = first + threadIdx.x;
@@ -570,59 +574,6 @@ __global__ void __launch_bounds__(kWalkThreads, walk_min_blocks<KB>()) walk_roun
         if (lane == leader) base = atomicAdd(a.wave_n_out, (unsigned long long)__popc(mask));
         base = __shfl_sync(0xffffffffu, base, leader);
         if (park) a.wave_out[base + __popc(mask & ((1u << lane) - 1u))] = qid;
-    }
-}
-
-// Wave round: every live query walks at most `trips` loop trips; walks that
-// end write their results, the others park (curr, prev) + their partial list
-// and are compacted (warp-ordered, so Morton neighbours stay together) into
-// the next round's list.  Lanes idle at most `trips` trips per round, with
-// no per-trip warp vote.  Grid-stride over a fixed persistent grid, because
-// the live count is only known on the device.  The last round's survivors
-// are the overflow pass's input.
-template <int D, int S, int KB, bool UNORDERED>
-__global__ void __launch_bounds__(256) walk_wave_kernel(const WalkArgs a) {
-    const bool first = a.wave_in == nullptr;
-    const int32_t items = first ? int32_t(a.m) : int32_t(*a.wave_n_in);
-    if (!first && a.resume_min > 0 && items < a.resume_min) return;  // few: the CTA pass takes them
-    const int32_t stride = int32_t(gridDim.x * blockDim.x);  // a multiple of 32
-    const unsigned lane = threadIdx.x & 31u;
-    // whole warps iterate together so the survivor ballot can use a full mask
-    for (int32_t wb = int32_t(blockIdx.x * blockDim.x + threadIdx.x) - int32_t(lane); wb < items;
-         wb += stride) {
-        const int32_t pos = wb + int32_t(lane);
-        LaneWalk<D, S, KB, false, UNORDERED> w;
-        bool active = false;
-        if (pos < items) {
-            if (first) {
-                active = w.init(a, pos);
-            } else {
-                w.resume(a, int32_t(a.wave_in[pos]));
-                active = true;
-            }
-        }
-        bool park = false;
-        if (active) {
-            if (a.n > 0) {
-                int t = a.trips;
-                while (w.step(a)) {
-                    if (--t == 0) {
-                        park = true;
-                        break;
-                    }
-                }
-            }
-            w.finish(a);
-            if (park) a.wave_state[w.qi] = make_int2(w.curr, w.prev);
-        }
-        const unsigned mask = __ballot_sync(0xffffffffu, park);
-        if (mask) {
-            const unsigned leader = __ffs(mask) - 1;
-            unsigned long long base = 0;
-            if (lane == leader) base = atomicAdd(a.wave_n_out, (unsigned long long)__popc(mask));
-            base = __shfl_sync(0xffffffffu, base, leader);
-            if (park) a.wave_out[base + __popc(mask & ((1u << lane) - 1u))] = uint32_t(w.qi);
-        }
     }
 }
 

@@ -13,19 +13,6 @@ inline unsigned walk_blocks(int64_t m, int threads) {
     return unsigned((m + threads - 1) / threads);
 }
 
-// Persistent grid: every SM filled to its occupancy limit, never more
-// blocks than the work needs.
-template <class K>
-unsigned persistent_blocks(K kernel, int64_t m) {
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, 0);
-    const int64_t full = int64_t(sms) * (per_sm > 0 ? per_sm : 1);
-    const int64_t need = (m + 255) / 256;
-    return unsigned(need < full ? need : full);
-}
-
 // Tail pass over the queries the walk kernel stopped (overflow.cuh); a
 // persistent grid reads the device-side overflow count, so no host sync.
 template <int D, int S, int KB>
@@ -47,19 +34,12 @@ void launch_one(const WalkArgs& a, cudaStream_t st) {
 }
 
 template <int D, int S, int KB, bool UNORDERED>
-void launch_wave(const WalkArgs& a, cudaStream_t st) {
-    auto kern = walk_wave_kernel<D, S, KB, UNORDERED>;
-    static const unsigned grid = persistent_blocks(kern, int64_t(1) << 40);
-    kern<<<grid, 256, 0, st>>>(a);
-}
-
-template <int D, int S, int KB, bool UNORDERED>
 void launch_round(const WalkArgs& a, cudaStream_t st) {
     walk_round_kernel<D, S, KB, UNORDERED><<<walk_blocks(a.m, kWalkThreads), kWalkThreads, 0, st>>>(a);
 }
 
 // phase 0: the walk kernel; phase 1: the overflow pass (when budgeted);
-// phase 2: one wave round (resume pass); phase 3: one continuation round.
+// phase 3: one continuation round or the resume pass.
 template <int D, int S, int KB>
 int launch_bucket(const WalkArgs& a, bool stats, bool unordered, int phase, cudaStream_t st) {
     if (phase == 1) {
@@ -72,13 +52,6 @@ int launch_bucket(const WalkArgs& a, bool stats, bool unordered, int phase, cuda
             launch_round<D, S, KB, true>(a, st);
         else
             launch_round<D, S, KB, false>(a, st);
-        return 1;
-    }
-    if (phase == 2) {
-        if (unordered)
-            launch_wave<D, S, KB, true>(a, st);
-        else
-            launch_wave<D, S, KB, false>(a, st);
         return 1;
     }
     if (stats) {
