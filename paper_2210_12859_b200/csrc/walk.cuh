@@ -107,18 +107,53 @@ __device__ __forceinline__ float pick(const float (&a)[D], int d) {
     return r;
 }
 
+// Packed FP32 pairs (sm_100: FADD2 / FMUL2, one instruction for two IEEE
+// round-to-nearest lanes, so every lane's bits equal the scalar op's).
+__device__ __forceinline__ uint64_t f2_pack(float lo, float hi) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ void f2_unpack(uint64_t v, float& lo, float& hi) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ uint64_t f2_sub(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ uint64_t f2_mul(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+
 // point.hpp:68-75: acc = 0; acc += (q_i - p_i)^2 left to right.  0 + x == x
-// for the non-negative first square, so the chain starts at it.
+// for the non-negative first square, so the chain starts at it.  The
+// differences and squares are formed two coordinates per instruction
+// (FADD2 / FMUL2, exact per lane); the sum stays the scalar left-to-right
+// chain, so the result is bit-identical to the reference's loop (for D = 3:
+// 6 instead of 8 FP instructions).
 template <int D>
 __device__ __forceinline__ float sq_dist(const float (&q)[D], const float (&p)[D]) {
-    float d0 = __fsub_rn(q[0], p[0]);
-    float acc = __fmul_rn(d0, d0);
+    if constexpr (D == 1) {
+        const float d0 = __fsub_rn(q[0], p[0]);
+        return __fmul_rn(d0, d0);
+    } else {
+        float acc = 0.0f;
 #pragma unroll
-    for (int i = 1; i < D; ++i) {
-        const float di = __fsub_rn(q[i], p[i]);
-        acc = __fadd_rn(acc, __fmul_rn(di, di));
+        for (int i = 0; i + 1 < D; i += 2) {
+            const uint64_t d = f2_sub(f2_pack(q[i], q[i + 1]), f2_pack(p[i], p[i + 1]));
+            float a, b;
+            f2_unpack(f2_mul(d, d), a, b);
+            acc = i == 0 ? __fadd_rn(a, b) : __fadd_rn(__fadd_rn(acc, a), b);
+        }
+        if constexpr (D % 2 == 1) {
+            const float dl = __fsub_rn(q[D - 1], p[D - 1]);
+            acc = __fadd_rn(acc, __fmul_rn(dl, dl));
+        }
+        return acc;
     }
-    return acc;
 }
 
 // Full point of one node.  S is the store stride: S in {2,4,8} is a padded
