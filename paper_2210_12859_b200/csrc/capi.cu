@@ -49,19 +49,30 @@ struct Tuning {
     int64_t resume_min = 0;  // 0: SMs x 64 (measured: 8-D and 4-D kNN64 tails; C3's ~2k stay on the CTA pass)
     int resume_trips = 0;    // 0: fcp 4096, kNN 12288 (measured on 8-D); <0: unbounded
     // continuation rounds after the budgeted walk (walk_round_kernel), trips
-    // per round.  Measured (tools/rounds_ab.sh, profiles/r01e_rounds_*): fcp
-    // walk -14% (3-D C3) to -30% (4-D), kNN4 4-D -18%; for lists of >= 8
-    // slots parking costs what the denser warps save (C3 kNN8 walk + tail
-    // 9.06 vs 9.03 ms, 4-D kNN20 +48%), so those keep one long budgeted walk.
-    std::vector<int> rounds_fcp{112, 224, 448}, rounds_knn{256, 512};
+    // per round.  Measured (tools/rounds_ab.sh, tools/rounds_knn_ab.sh,
+    // profiles/r01e_rounds_*): fcp walk -14% (3-D C3) to -30% (4-D), kNN4
+    // 4-D -18%, kNN8 walk + tail -3% (C3) / -7% (4-D) / +1% (3-D uniform);
+    // for lists of >= 16 slots parking costs more than the denser warps save
+    // (2-D kNN16 +2%, 4-D kNN20 +48%), so those keep one long budgeted walk.
+    std::vector<int> rounds_fcp{112, 224, 448}, rounds_knn4{256, 512}, rounds_knn8{384, 768, 1536};
+    std::vector<int> rounds_knn_env;
     bool rounds_knn_all = false;  // FKD_RROUNDS_KNN given: every kNN bucket
 };
 
 int walk_bucket_of(int k);
-// the rounds run for register lists of <= 4 slots (fcp, k <= 4)
-inline bool rounds_on(int k) { return walk_bucket_of(k) <= 4; }
+// The rounds run for register lists of <= 4 slots (fcp, k <= 4) and, in
+// batches of >= 2^22 queries, 8 slots (a 1M-query kNN8 batch is 4-8% slower
+// with them: the round boundaries cost more than the small batch's warps lose).
+inline bool rounds_on(int k, int64_t m) {
+    const int kb = walk_bucket_of(k);
+    return kb <= 4 || (kb == 8 && m >= (int64_t(1) << 22));
+}
 // first walk's loop trips before a query parks (FKD_BUDGET < 0: per kind)
-inline int first_budget(int k) { return k == 1 ? 112 : (rounds_on(k) ? 256 : 3072); }
+inline int first_budget(int k, int64_t m) {
+    if (k == 1) return 112;
+    if (!rounds_on(k, m)) return 3072;
+    return walk_bucket_of(k) <= 4 ? 256 : 384;
+}
 // resume pass trips (FKD_RESUME_TRIPS = 0): 4 x the per-kind budget without rounds
 inline int resume_trips_default(int k) { return 4 * (k == 1 ? 1024 : 3072); }
 
@@ -89,7 +100,7 @@ Tuning tuning() {
         if (const char* e = std::getenv("FKD_RESUME_TRIPS")) x.resume_trips = std::atoi(e);
         if (const char* e = std::getenv("FKD_RROUNDS_FCP")) x.rounds_fcp = parse_ints(e);
         if (const char* e = std::getenv("FKD_RROUNDS_KNN")) {
-            x.rounds_knn = parse_ints(e);
+            x.rounds_knn_env = parse_ints(e);
             x.rounds_knn_all = true;
         }
         return x;
@@ -485,7 +496,7 @@ fkd_status enqueue(const fkd_tree* t, Replica& r, Workspace* w, const float* d_q
         a.bad = w->small;
         a.id_base = id_offset + base;
         const Tuning tu = tuning();
-        int budget = tu.budget >= 0 ? tu.budget : first_budget(k);
+        int budget = tu.budget >= 0 ? tu.budget : first_budget(k, cm);
         if (budget_div > 1 && budget > 0) budget = std::max(64, budget / budget_div);
         a.budget = (stats || walk_bucket_of(k) == 0 || t->dim > 8) ? 0 : budget;
         if (a.budget > 0) {
@@ -528,7 +539,10 @@ fkd_status enqueue(const fkd_tree* t, Replica& r, Workspace* w, const float* d_q
             const cudaStream_t ts = (a.budget > 0 && tail_st) ? tail_st : st;
             static const std::vector<int> none;
             const std::vector<int>& rounds =
-                k == 1 ? tu.rounds_fcp : ((rounds_on(k) || tu.rounds_knn_all) ? tu.rounds_knn : none);
+                k == 1 ? tu.rounds_fcp
+                       : (tu.rounds_knn_all ? tu.rounds_knn_env
+                                            : (!rounds_on(k, cm) ? none
+                                                             : (walk_bucket_of(k) <= 4 ? tu.rounds_knn4 : tu.rounds_knn8)));
             if (a.budget > 0 && !rounds.empty()) {
                 // continuation rounds: the parked walks, compacted into dense
                 // warps, continue for `trips` more trips per round; lists

@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(THREADS) overflow_kernel(const WalkArgs a) {
         __syncthreads();
 
         auto consider = [&](int32_t node, const float (&p)[D]) {
-            const float d2 = sq_dist(q, p);
+            const float d2 = sq_dist<D, (D <= 4 && KB <= 8)>(q, p);
             const uint64_t key = make_key(d2, node);
             if (d2 <= cap2 && key < L[KB - 1]) {
                 list_insert(L, key);

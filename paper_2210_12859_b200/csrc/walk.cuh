@@ -134,11 +134,22 @@ __device__ __forceinline__ uint64_t f2_mul(uint64_t a, uint64_t b) {
 // (FADD2 / FMUL2, exact per lane); the sum stays the scalar left-to-right
 // chain, so the result is bit-identical to the reference's loop (for D = 3:
 // 6 instead of 8 FP instructions).
-template <int D>
+//
+// Pairs are used for D <= 4 with lists of <= 8 slots (PAIRS): with longer
+// lists or more coordinates the pair registers cost more than they save
+// (measured: 4-D kNN20 walk +12%, the 8-D kNN16 CTA pass drops to one CTA
+// per SM).  Both forms give the same bits, so callers may mix them.
+template <int D, bool PAIRS = (D <= 4)>
 __device__ __forceinline__ float sq_dist(const float (&q)[D], const float (&p)[D]) {
-    if constexpr (D == 1) {
-        const float d0 = __fsub_rn(q[0], p[0]);
-        return __fmul_rn(d0, d0);
+    if constexpr (!PAIRS || D == 1) {
+        float d0 = __fsub_rn(q[0], p[0]);
+        float acc = __fmul_rn(d0, d0);
+#pragma unroll
+        for (int i = 1; i < D; ++i) {
+            const float di = __fsub_rn(q[i], p[i]);
+            acc = __fadd_rn(acc, __fmul_rn(di, di));
+        }
+        return acc;
     } else {
         float acc = 0.0f;
 #pragma unroll
@@ -323,14 +334,14 @@ struct LaneWalk {
             // traverse.hpp:217-222.  kNN: the distance is computed every trip
             // (no divergent block; measured faster), admission is predicated
             // on a first visit.
-            const float d2 = sq_dist(q, p);
+            const float d2 = sq_dist<D, (D <= 4 && KB <= 8)>(q, p);
             const uint64_t key = make_key(d2, curr);
             if (from_parent && key_lt(key, L[KB - 1])) {  // d2 <= cap2 and beats the kth (cap_key)
                 list_insert(L, key);
                 r2 = key_dist(L[KB - 1]);
             }
         } else if (from_parent) {  // fcp: a branch is cheaper than 8 more FP ops
-            const float d2 = sq_dist(q, p);
+            const float d2 = sq_dist<D, (D <= 4)>(q, p);
             const uint64_t key = make_key(d2, curr);
             if (key_lt(key, L[KB - 1])) {  // d2 <= cap2 and beats the best (cap_key)
                 list_insert(L, key);
