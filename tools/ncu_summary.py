@@ -26,9 +26,12 @@ WANT = {
     "sm__cycles_elapsed.avg": "sm_elapsed_cycles",
     "launch__grid_size": "grid",
     "launch__block_size": "block",
+    "lts__t_sectors.sum": "l2_sectors",
+    "lts__throughput.avg.pct_of_peak_sustained_elapsed": "l2_throughput_pct",
+    "l1tex__throughput.avg.pct_of_peak_sustained_elapsed": "l1_throughput_pct",
 }
 UNIT = {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "byte": 1, "usecond": 1e-6, "msecond": 1e-3,
-        "nsecond": 1e-9, "second": 1}
+        "nsecond": 1e-9, "second": 1, "us": 1e-6, "ms": 1e-3, "ns": 1e-9, "s": 1}
 
 
 def main(path):
@@ -51,6 +54,14 @@ def main(path):
             rec["sectors_per_request"] = rec["ld_sectors"] / rec["ld_requests"]
         if rec.get("sm_elapsed_cycles"):
             rec["sm_active_frac"] = rec["sm_active_cycles"] / rec["sm_elapsed_cycles"]
+        # duration is in seconds (ncu mixes ms / us units per kernel)
+        if isinstance(rec.get("duration"), float) and rec["duration"] > 0:
+            rec["duration_ms"] = rec["duration"] * 1e3
+            if "dram_traffic_bytes" in rec:
+                rec["dram_gbs"] = rec["dram_traffic_bytes"] / rec["duration"] / 1e9
+            if isinstance(rec.get("l2_sectors"), float):
+                rec["l2_bytes"] = rec["l2_sectors"] * 32
+                rec["l2_gbs"] = rec["l2_bytes"] / rec["duration"] / 1e9
         print(json.dumps(rec))
 
 
