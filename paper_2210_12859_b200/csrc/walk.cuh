@@ -330,17 +330,19 @@ struct LaneWalk {
             load_point<D, S>(a.nodes, curr, p);
             pd = pick(p, d);
         }
-        if constexpr (KB > 1) {
-            // traverse.hpp:217-222.  kNN: the distance is computed every trip
-            // (no divergent block; measured faster), admission is predicated
-            // on a first visit.
+        if constexpr (KB > 1 || D == 3) {
+            // traverse.hpp:217-222.  kNN, and 3-D fcp: the distance is
+            // computed every trip (no divergent block; measured faster: fcp
+            // 3-D -3.6% with the packed-pair distance, but 4-D +22%, and the
+            // 2-D fcp walk would take 44 instead of 28 registers),
+            // admission is predicated on a first visit.
             const float d2 = sq_dist<D, (D <= 4 && KB <= 8)>(q, p);
             const uint64_t key = make_key(d2, curr);
             if (from_parent && key_lt(key, L[KB - 1])) {  // d2 <= cap2 and beats the kth (cap_key)
                 list_insert(L, key);
                 r2 = key_dist(L[KB - 1]);
             }
-        } else if (from_parent) {  // fcp: a branch is cheaper than 8 more FP ops
+        } else if (from_parent) {  // fcp, D != 3: a branch is cheaper than the FP ops
             const float d2 = sq_dist<D, (D <= 4)>(q, p);
             const uint64_t key = make_key(d2, curr);
             if (key_lt(key, L[KB - 1])) {  // d2 <= cap2 and beats the best (cap_key)
