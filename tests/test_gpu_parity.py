@@ -517,3 +517,28 @@ def test_host_buffers_pinned_and_pageable(oracle, mode, monkeypatch):
         fk.run_batch_device(tree, dq, c, h, fk.BatchOptions(kind=kind, k=k))
         assert np.array_equal(got_c, c.cpu().numpy())
         assert np.array_equal(got_h, h.cpu().numpy())
+
+
+def test_knn8_rounds_large_batch(oracle):
+    """kNN8 batches of >= 2^22 queries take the continuation rounds (capi.cu
+    rounds_on); the same queries through the host pipeline's chunks (< 2^22
+    each: one budgeted walk) and the oracle on a sample must give the same bytes."""
+    import torch
+    pts = fk.clustered_points(8, 1, 300_000, 3)
+    m = (1 << 22) + 1000
+    qs = fk.clustered_points(8, 2, m, 3)
+    nodes = fk.build_level_order(pts)
+    tree = fk.KdTree.from_level_order(nodes)
+    for k in (8, 5):
+        opt = fk.BatchOptions(kind=fk.QueryKind.knn, k=k)
+        dq = torch.from_numpy(qs).cuda()
+        c = torch.empty(m, dtype=torch.int32, device="cuda")
+        h = torch.empty(m * k, dtype=torch.int64, device="cuda")
+        fk.run_batch_device(tree, dq, c, h, opt)
+        res = fk.run_batch(tree, qs, opt)
+        assert np.array_equal(c.cpu().numpy(), res.counts)
+        assert h.cpu().numpy().tobytes() == res.hits.tobytes()
+        sample = np.arange(0, m, 211)
+        rc, rh = oracle.run_batch(nodes, qs[sample], "knn", k, INF)[:2]
+        assert np.array_equal(res.counts[sample], rc)
+        assert res.hits.reshape(m, -1)[sample].tobytes() == rh.reshape(len(sample), -1).tobytes()
