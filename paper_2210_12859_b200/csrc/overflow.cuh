@@ -97,7 +97,10 @@ __global__ void __launch_bounds__(THREADS) overflow_kernel(const WalkArgs a) {
         if (tid == 0) {
             // bound from the partial list the walk kernel left in the slot
             float b = cap2;
-            if (a.counts[qi] == k) b = fminf(b, a.hits[qi * k + (k - 1)].dist2);
+            // (a full partial list: its last slot holds a hit; the walk does not
+            // write the count of a parked query)
+            const fkd_hit last = a.hits[qi * k + (k - 1)];
+            if (last.node >= 0) b = fminf(b, last.dist2);
             r2_bits = __float_as_uint(b);
             frontier[0][0] = 0;
             fcount[0] = 1;

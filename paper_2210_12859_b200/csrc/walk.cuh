@@ -460,8 +460,10 @@ struct LaneWalk {
         cnt = Counters<STATS>();
     }
 
-    // fixed-stride slot in input order (batch.cpp:104-119)
-    __device__ __forceinline__ void finish(const WalkArgs& a) {
+    // fixed-stride slot in input order (batch.cpp:104-119).  A parked walk
+    // (final = false) leaves only its partial list: the passes that continue
+    // it read the list, never the count, which its last finish writes.
+    __device__ __forceinline__ void finish(const WalkArgs& a, bool final = true) {
         const int k = a.k;
         const int dummies = KB - k;
         int2* out = reinterpret_cast<int2*>(a.hits + qi * k);
@@ -477,7 +479,7 @@ struct LaneWalk {
                 c += hit;
             }
         }
-        a.counts[qi] = c;
+        if (final) a.counts[qi] = c;
         if constexpr (STATS) {
             if (a.per_query) {
                 unsigned long long s = cnt.steps, v = cnt.visited;
@@ -576,7 +578,7 @@ __global__ void __launch_bounds__(kWalkThreads, walk_min_blocks<KB>()) walk_kern
                 over = walk_budgeted(w, a, a.budget);
             }
         }
-        w.finish(a);  // over budget: the partial list stays as the overflow pass's bound
+        w.finish(a, !over);  // over budget: the partial list stays as the overflow pass's bound
         if (over) {
             a.ovf_ids[atomicAdd(a.ovf_count, 1ull)] = uint32_t(w.qi);
             a.wave_state[w.qi] = make_int2(w.curr, w.prev);  // for the resume pass
@@ -611,7 +613,7 @@ __global__ void __launch_bounds__(kWalkThreads, walk_min_blocks<KB>()) walk_roun
         qid = a.wave_in[i];
         w.resume(a, int32_t(qid));
         park = walk_budgeted(w, a, a.trips);
-        w.finish(a);
+        w.finish(a, !park);
         if (park) a.wave_state[qid] = make_int2(w.curr, w.prev);
     }
     const unsigned lane = threadIdx.x & 31u;
