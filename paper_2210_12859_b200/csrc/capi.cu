@@ -107,9 +107,9 @@ Tuning tuning() {
     }();
 }
 
-// Store layout: padded vectors (1, 2, 4, 4, 8, 8, 8, 8 floats) by default;
-// FKD_LAYOUT=packed keeps 3-D nodes at 12 bytes (chosen
-// by measurement).
+// Store layout: padded vectors (1, 4, 4, 4, 8, 8, 8, 8 floats) by default;
+// FKD_LAYOUT=packed keeps 2-D and 3-D nodes at 8 and 12 bytes (SURVEY §7
+// step 3: chosen by measurement).
 int store_stride(int dim) {
     static const bool packed = [] {
         const char* e = std::getenv("FKD_LAYOUT");
@@ -117,7 +117,7 @@ int store_stride(int dim) {
     }();
     switch (dim) {
         case 1: return 1;
-        case 2: return 2;
+        case 2: return packed ? 2 : 4;  // 16-byte nodes with the split plane: 2-D kNN16 -1%, fcp -3%
         case 3: return packed ? 3 : 4;
         case 4: return 4;
         case 5: case 6: case 7: case 8: return 8;
