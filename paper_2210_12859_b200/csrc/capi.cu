@@ -47,7 +47,7 @@ constexpr int64_t kSortChunk = int64_t(1) << 30;  // u32 ids, int item counts in
 struct Tuning {
     int budget = -1;  // -1: per kind (first_budget: fcp 112, kNN <= 4 slots 256, larger lists 3072 loop trips)
     int64_t resume_min = 0;  // 0: SMs x 64 (measured: 8-D and 4-D kNN64 tails; C3's ~2k stay on the CTA pass)
-    int resume_trips = 0;    // 0: fcp 4096, kNN 12288 (measured on 8-D); <0: unbounded
+    int resume_trips = 0;    // 0: fcp 4096, kNN 49152 (measured on 8-D); <0: unbounded
     // continuation rounds after the budgeted walk (walk_round_kernel), trips
     // per round.  Measured (tools/rounds_ab.sh, tools/rounds_knn_ab.sh,
     // profiles/r01e_rounds_*): fcp walk -14% (3-D C3) to -30% (4-D), kNN4
@@ -74,7 +74,9 @@ inline int first_budget(int k, int64_t m) {
     return walk_bucket_of(k) <= 4 ? 256 : 384;
 }
 // resume pass trips (FKD_RESUME_TRIPS = 0): 4 x the per-kind budget without rounds
-inline int resume_trips_default(int k) { return 4 * (k == 1 ? 1024 : 3072); }
+// kNN: 8-D kNN16 (C4) 12288 -> 49152 cuts the CTA pass 269 -> 61 ms and the batch 353 -> 318 ms;
+// 4-D kNN16/50/64 and 5-D kNN16 finish inside 12288 (unchanged); tools/tail8d_ab2.sh
+inline int resume_trips_default(int k) { return k == 1 ? 4096 : 49152; }
 
 std::vector<int> parse_ints(const char* e) {
     std::vector<int> v;
