@@ -526,6 +526,14 @@ __device__ __forceinline__ void add_totals(const WalkArgs& a, unsigned long long
 #ifndef FKD_MINB_KB16
 #define FKD_MINB_KB16 1
 #endif
+// 5-D and 8-D, 16 slots: 4 blocks (64 registers, 16 B of stack in 8-D)
+// instead of 3 (72 registers): the 8-D walk is long-scoreboard bound at 24
+// warps/SM; kNN16 M=1M 8-D 318 -> 298 ms, 5-D -3.5%, while 6-D (+4%), 7-D
+// (+0.5%) and 2-D/3-D/4-D (+0.4-0.8%) lose that way (tools/occ16_ab.sh,
+// tools/occ16_hd_ab.sh, profiles/r01i_occ16_*ab.log)
+#ifndef FKD_MINB_KB16_HIGH_D
+#define FKD_MINB_KB16_HIGH_D 4
+#endif
 // Threads per walk block: a block's slot stays held until its slowest warp
 // ends, so smaller blocks waste less occupancy on budget-capped stragglers.
 #ifndef FKD_WALK_T
@@ -533,9 +541,9 @@ __device__ __forceinline__ void add_totals(const WalkArgs& a, unsigned long long
 #endif
 constexpr int kWalkThreads = FKD_WALK_T;
 
-template <int KB>
+template <int D, int KB>
 constexpr int walk_min_blocks() {
-    return KB == 8 ? FKD_MINB_KB8 : (KB == 16 ? FKD_MINB_KB16 : 1);
+    return KB == 8 ? FKD_MINB_KB8 : (KB == 16 ? ((D == 5 || D == 8) ? FKD_MINB_KB16_HIGH_D : FKD_MINB_KB16) : 1);
 }
 
 // Walks until the root exits (false) or about `trips` loop trips have run
@@ -570,7 +578,7 @@ __device__ __forceinline__ bool walk_budgeted(W& w, const WalkArgs& a, int trips
 
 // One thread per walk position (plain grid).
 template <int D, int S, int KB, bool STATS, bool UNORDERED>
-__global__ void __launch_bounds__(kWalkThreads, walk_min_blocks<KB>()) walk_kernel(const WalkArgs a) {
+__global__ void __launch_bounds__(kWalkThreads, walk_min_blocks<D, KB>()) walk_kernel(const WalkArgs a) {
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     LaneWalk<D, S, KB, STATS, UNORDERED> w;
     bool active = i < a.m && w.init(a, i);
@@ -609,7 +617,7 @@ __global__ void __launch_bounds__(kWalkThreads, walk_min_blocks<KB>()) walk_kern
 // at least that many walks are parked (bulk long walks, e.g. 8-D), else the
 // CTA pass takes them all (overflow.cuh reads the same count).
 template <int D, int S, int KB, bool UNORDERED>
-__global__ void __launch_bounds__(kWalkThreads, walk_min_blocks<KB>()) walk_round_kernel(const WalkArgs a) {
+__global__ void __launch_bounds__(kWalkThreads, walk_min_blocks<D, KB>()) walk_round_kernel(const WalkArgs a) {
     const int64_t items = int64_t(*a.wave_n_in);
     if (a.resume_min > 0 && items < a.resume_min) return;
     const int64_t first = int64_t(blockIdx.x) * blockDim.x;
