@@ -263,6 +263,12 @@ __device__ __forceinline__ int dim_down(int d) {  // split dim one level up
     else return d == 0 ? D - 1 : d - 1;
 }
 
+// Lowest dimension whose 16-slot walks keep the list in the output slot
+// (LaneWalk::kSlot); 9 turns the mode off.
+#ifndef FKD_SLOT_LIST_MIN_D
+#define FKD_SLOT_LIST_MIN_D 8
+#endif
+
 template <int D, int S, int KB, bool STATS, bool UNORDERED>
 struct LaneWalk {
     // With a split-plane slot in the store (S > D) the walk never needs the
@@ -271,9 +277,15 @@ struct LaneWalk {
     static constexpr bool kRot = S > D && D > 1;
     static constexpr int kKB = KB;
     static constexpr int kD = D;
+    // Slot-list mode (high dimensions, 16 slots): the sorted list lives in the
+    // query's own output slot (Hit format, k entries) and only its kth key is
+    // a register.  In 8-D a query processes ~15k nodes for ~100 admissions,
+    // so the 32 list registers buy nothing but cost occupancy in a walk that
+    // is load-latency bound.
+    static constexpr bool kSlot = D >= FKD_SLOT_LIST_MIN_D && KB == 16;
     float q[D];
     float qr[kRot ? D : 1];
-    uint64_t L[KB];
+    uint64_t L[kSlot ? 1 : KB];  // slot mode: L[0] is the kth key
     int32_t curr, prev;
     int d;  // split dim of curr, tracked incrementally (tree.hpp:27-29)
     float r2;
@@ -299,10 +311,16 @@ struct LaneWalk {
 #pragma unroll
             for (int j = 0; j < D; ++j) qr[j] = q[j];  // depth 0 splits dim 0
         }
-        const int dummies = KB - a.k;
         const uint64_t empty = cap_key(a.cap2);
+        if constexpr (kSlot) {
+            int2* out = reinterpret_cast<int2*>(a.hits + qi * a.k);
+            for (int j = 0; j < a.k; ++j) out[j] = make_int2(-1, 0x7f800000);  // Hit{-1, +inf}
+            L[0] = empty;
+        } else {
+            const int dummies = KB - a.k;
 #pragma unroll
-        for (int j = 0; j < KB; ++j) L[j] = j < dummies ? 0ull : empty;
+            for (int j = 0; j < KB; ++j) L[j] = j < dummies ? 0ull : empty;
+        }
         curr = 0;
         prev = -1;
         d = 0;
@@ -339,7 +357,12 @@ struct LaneWalk {
             // admission is predicated on a first visit.
             const float d2 = sq_dist<D, (D <= 4 && KB <= 8)>(q, p);
             const uint64_t key = make_key(d2, curr);
-            if (from_parent && key_lt(key, L[KB - 1])) {  // d2 <= cap2 and beats the kth (cap_key)
+            if constexpr (kSlot) {
+                if (from_parent && key_lt(key, L[0])) {
+                    slot_insert(a, key);
+                    r2 = key_dist(L[0]);
+                }
+            } else if (from_parent && key_lt(key, L[KB - 1])) {  // d2 <= cap2 and beats the kth (cap_key)
                 list_insert(L, key);
                 r2 = key_dist(L[KB - 1]);
             }
@@ -416,6 +439,28 @@ struct LaneWalk {
         return true;
     }
 
+    // Sorted insertion into the output slot (slot mode): x passes the
+    // entries it does not beat, then displaces each later one by one; the
+    // old kth drops out.  Entries are converted as in resume() / finish().
+    __device__ __forceinline__ void slot_insert(const WalkArgs& a, uint64_t x) {
+        const int k = a.k;
+        const uint64_t empty = cap_key(a.cap2);
+        int2* out = reinterpret_cast<int2*>(a.hits + qi * k);
+        uint64_t last = x;
+        for (int j = 0; j < k; ++j) {
+            const int2 h = out[j];
+            const uint64_t kj = h.x < 0 ? empty : (uint64_t(uint32_t(h.y) + 1u) << 32) | uint32_t(h.x);
+            last = kj;
+            if (key_lt(x, kj)) {
+                const bool hit = uint32_t(x) != 0xFFFFFFFFu;
+                out[j] = make_int2(int32_t(uint32_t(x)), hit ? int32_t(uint32_t(x >> 32) - 1u) : 0x7f800000);
+                last = x;
+                x = kj;
+            }
+        }
+        L[0] = last;
+    }
+
     // Resumes a walk parked by an earlier pass (walk budget or round): the state is the
     // reference's two node ids; the candidate list is the partial one the
     // round left in the query's own output slot; radius2 and the split
@@ -428,16 +473,21 @@ struct LaneWalk {
         const int dummies = KB - a.k;
         const uint64_t empty = cap_key(a.cap2);
         const int2* slot = reinterpret_cast<const int2*>(a.hits + size_t(qi) * a.k);
+        if constexpr (kSlot) {
+            const int2 h = slot[a.k - 1];  // the list stays in the slot; only its kth is a register
+            L[0] = h.x < 0 ? empty : (uint64_t(uint32_t(h.y) + 1u) << 32) | uint32_t(h.x);
+        } else {
 #pragma unroll
-        for (int j = 0; j < KB; ++j) {
-            if (j < dummies) {
-                L[j] = 0ull;
-            } else {
-                const int2 h = slot[j - dummies];
-                L[j] = h.x < 0 ? empty : (uint64_t(uint32_t(h.y) + 1u) << 32) | uint32_t(h.x);
+            for (int j = 0; j < KB; ++j) {
+                if (j < dummies) {
+                    L[j] = 0ull;
+                } else {
+                    const int2 h = slot[j - dummies];
+                    L[j] = h.x < 0 ? empty : (uint64_t(uint32_t(h.y) + 1u) << 32) | uint32_t(h.x);
+                }
             }
         }
-        r2 = key_dist(L[KB - 1]);
+        r2 = key_dist(L[kSlot ? 0 : KB - 1]);
         const int2 st = a.wave_state[qi];
         curr = st.x;
         prev = st.y;
@@ -469,15 +519,26 @@ struct LaneWalk {
         const int dummies = KB - k;
         int2* out = reinterpret_cast<int2*>(a.hits + qi * k);
         int c = 0;
+        if constexpr (kSlot) {
+            // the slot already holds the list; count its hits (all k once the kth is one)
+            if (final) {
+                if (uint32_t(L[0]) != 0xFFFFFFFFu) {
+                    c = k;
+                } else {
+                    for (int j = 0; j < k; ++j) c += out[j].x >= 0;
+                }
+            }
+        } else {
 #pragma unroll
-        for (int j = 0; j < KB; ++j) {
-            const int s = j - dummies;
-            if (s >= 0) {
-                const uint64_t key = L[j];
-                const bool hit = uint32_t(key) != 0xFFFFFFFFu;  // empty slot -> Hit{-1, +inf}
-                out[s] = make_int2(int32_t(uint32_t(key)),
-                                   hit ? int32_t(uint32_t(key >> 32) - 1u) : 0x7f800000);
-                c += hit;
+            for (int j = 0; j < KB; ++j) {
+                const int s = j - dummies;
+                if (s >= 0) {
+                    const uint64_t key = L[j];
+                    const bool hit = uint32_t(key) != 0xFFFFFFFFu;  // empty slot -> Hit{-1, +inf}
+                    out[s] = make_int2(int32_t(uint32_t(key)),
+                                       hit ? int32_t(uint32_t(key >> 32) - 1u) : 0x7f800000);
+                    c += hit;
+                }
             }
         }
         if (final) a.counts[qi] = c;
@@ -534,6 +595,13 @@ __device__ __forceinline__ void add_totals(const WalkArgs& a, unsigned long long
 #ifndef FKD_MINB_KB16_HIGH_D
 #define FKD_MINB_KB16_HIGH_D 4
 #endif
+// 16-slot walks whose list lives in the output slot (LaneWalk::kSlot, 8-D):
+// 5 blocks (48 registers, 40 B of spill stores) -> 8-D kNN16 walk 300 -> 281 ms;
+// 4 blocks 300 ms, 6 blocks (40 registers) 295 ms (tools/slot_ab.sh,
+// profiles/r01i_slot_ab.log)
+#ifndef FKD_MINB_KB16_SLOT
+#define FKD_MINB_KB16_SLOT 5
+#endif
 // Threads per walk block: a block's slot stays held until its slowest warp
 // ends, so smaller blocks waste less occupancy on budget-capped stragglers.
 #ifndef FKD_WALK_T
@@ -543,7 +611,9 @@ constexpr int kWalkThreads = FKD_WALK_T;
 
 template <int D, int KB>
 constexpr int walk_min_blocks() {
-    return KB == 8 ? FKD_MINB_KB8 : (KB == 16 ? ((D == 5 || D == 8) ? FKD_MINB_KB16_HIGH_D : FKD_MINB_KB16) : 1);
+    return KB == 8 ? FKD_MINB_KB8 : (KB == 16 ? (D >= FKD_SLOT_LIST_MIN_D ? FKD_MINB_KB16_SLOT
+                                             : (D == 5 || D == 8) ? FKD_MINB_KB16_HIGH_D : FKD_MINB_KB16)
+                       : 1);
 }
 
 // Walks until the root exits (false) or about `trips` loop trips have run

@@ -542,3 +542,34 @@ def test_knn8_rounds_large_batch(oracle):
         rc, rh = oracle.run_batch(nodes, qs[sample], "knn", k, INF)[:2]
         assert np.array_equal(res.counts[sample], rc)
         assert res.hits.reshape(m, -1)[sample].tobytes() == rh.reshape(len(sample), -1).tobytes()
+
+
+@pytest.mark.parametrize("budget,resume_min,resume_trips,rounds", [
+    ("-1", "0", "0", "-"), ("0", "0", "0", "-"),    # defaults; no budget (one walk, STATS too)
+    ("3", "0", "0", "0"), ("40", "1", "5", "0"),    # CTA pass; budgeted resume -> CTA pass
+    ("2", "1", "-1", "0"), ("2", "0", "0", "1,2"),  # unbounded resume; rounds -> CTA pass
+])
+def test_slot_list_walk_high_dim(oracle, budget, resume_min, resume_trips, rounds, monkeypatch):
+    """8-D walks with 16 slots keep their sorted list in the output slot
+    (LaneWalk::kSlot): insertion, parking, resuming, the CTA pass's bound and
+    the final count all go through the slot.  Runtime k below the bucket
+    (9, 12), bounded radii (short lists), grid-snapped ties, duplicates."""
+    monkeypatch.setenv("FKD_BUDGET", budget)
+    monkeypatch.setenv("FKD_RESUME_TRIPS", resume_trips)
+    monkeypatch.setenv("FKD_RESUME_MIN", resume_min if resume_min != "0" else str(1 << 40))
+    if rounds != "-":
+        monkeypatch.setenv("FKD_RROUNDS_KNN", rounds)
+    rng = oracle.instance_rng(8088)
+    for t in range(6):
+        n = (0, 1, 17, 3000, 6000, 12000)[t]
+        pts = rng.random_point_set(n, 8, 8 if t % 2 else 0, 0.2 if t % 3 == 0 else 0.0)
+        nodes = oracle.build_tree(pts) if n else pts
+        qs = np.stack([rng.random_query(8, pts) for _ in range(400)])
+        for k in (9, 12, 16):
+            for r in (INF, 0.6, 0.0):
+                res, ref = _run_both(oracle, nodes.reshape(n, 8), qs, k, r, morton=bool(t % 2))
+                _assert_same(res, ref, f"n={n} k={k} r={r} budget={budget}")
+                tree = fk.KdTree.from_level_order(nodes.reshape(n, 8))
+                fast = fk.run_batch(tree, qs, fk.BatchOptions(kind=fk.QueryKind.knn, k=k, max_radius=r))
+                assert np.array_equal(fast.counts, ref[0]) and fast.hits.tobytes() == ref[1].tobytes(), \
+                    f"budgeted n={n} k={k} r={r} budget={budget}"
