@@ -55,6 +55,13 @@ struct Tuning {
     // for lists of >= 16 slots parking costs more than the denser warps save
     // (2-D kNN16 +2%, 4-D kNN20 +48%), so those keep one long budgeted walk.
     std::vector<int> rounds_fcp{112, 224, 448}, rounds_knn4{256, 512}, rounds_knn8{384, 768, 1536};
+    // fcp batches below 2^22 queries stop after two rounds: their few parked walks
+    // finish sooner in the CTA pass than in a latency-bound 448-trip round
+    // (clustered 1.25M / 2.5M: -22% / -13%; 1M uniform -1%), while at 10M the third
+    // round keeps the resume pass off (C3 fcp 2.49 vs 3.03 ms without it)
+    // (tools/fcp_small_ab.sh, tools/fcp_rounds_c3_ab.sh, profiles/r01i_fcp_*ab.log)
+    std::vector<int> rounds_fcp_small{112, 224};
+    bool rounds_fcp_env = false;  // FKD_RROUNDS_FCP given: every batch size
     std::vector<int> rounds_knn_env;
     bool rounds_knn_all = false;  // FKD_RROUNDS_KNN given: every kNN bucket
 };
@@ -100,7 +107,10 @@ Tuning tuning() {
         if (const char* e = std::getenv("FKD_BUDGET")) x.budget = std::atoi(e);  // <0: per kind, 0: off
         if (const char* e = std::getenv("FKD_RESUME_MIN")) x.resume_min = std::atoll(e);
         if (const char* e = std::getenv("FKD_RESUME_TRIPS")) x.resume_trips = std::atoi(e);
-        if (const char* e = std::getenv("FKD_RROUNDS_FCP")) x.rounds_fcp = parse_ints(e);
+        if (const char* e = std::getenv("FKD_RROUNDS_FCP")) {
+            x.rounds_fcp = parse_ints(e);
+            x.rounds_fcp_env = true;
+        }
         if (const char* e = std::getenv("FKD_RROUNDS_KNN")) {
             x.rounds_knn_env = parse_ints(e);
             x.rounds_knn_all = true;
@@ -541,7 +551,7 @@ fkd_status enqueue(const fkd_tree* t, Replica& r, Workspace* w, const float* d_q
             const cudaStream_t ts = (a.budget > 0 && tail_st) ? tail_st : st;
             static const std::vector<int> none;
             const std::vector<int>& rounds =
-                k == 1 ? tu.rounds_fcp
+                k == 1 ? ((tu.rounds_fcp_env || cm >= (int64_t(1) << 22)) ? tu.rounds_fcp : tu.rounds_fcp_small)
                        : (tu.rounds_knn_all ? tu.rounds_knn_env
                                             : (!rounds_on(k, cm) ? none
                                                              : (walk_bucket_of(k) <= 4 ? tu.rounds_knn4 : tu.rounds_knn8)));

@@ -12,7 +12,7 @@ hq = fk.LIB.fkd_host_alloc(qs.nbytes); C.memmove(hq, qs.ctypes.data, qs.nbytes)
 bufs = {k: (fk.LIB.fkd_host_alloc(m * 4), fk.LIB.fkd_host_alloc(m * k * 8)) for k in (1, 8)}
 base = dict(os.environ)
 for spec in [""] + sys.argv[1:]:
-    env = dict(kv.split("=") for kv in spec.split(",") if kv)
+    env = dict(kv.split("=", 1) for kv in spec.split(";" if ";" in spec else ",") if kv)  # ";" separates knobs whose values hold commas
     os.environ.clear(); os.environ.update(base); os.environ.update(env)
     rec = {"knobs": spec or "default"}
     for kind, k in (("fcp", 1), ("knn", 8)):
