@@ -1024,6 +1024,15 @@ fkd_status fkd_run_batch(const fkd_tree* t, const float* queries, int64_t m, int
         const char* e = std::getenv("FKD_STREAMS");
         return e ? std::max(1, std::atoi(e)) : 4;
     }();
+    // ramp depths (FKD_RAMP_HEAD / FKD_RAMP_TAIL: experiment knobs)
+    const int ramp_head = [] {
+        const char* e = std::getenv("FKD_RAMP_HEAD");
+        return e ? std::max(0, std::min(6, std::atoi(e))) : 2;
+    }();
+    const int ramp_tail = [] {
+        const char* e = std::getenv("FKD_RAMP_TAIL");
+        return e ? std::max(0, std::min(6, std::atoi(e))) : 2;
+    }();
     const int64_t full_chunk = chunk_env
         ? std::max<int64_t>(1024, std::atoll(chunk_env))
         : std::min<int64_t>(int64_t(4) << 20,
@@ -1034,16 +1043,23 @@ fkd_status fkd_run_batch(const fkd_tree* t, const float* queries, int64_t m, int
             for (int64_t b = 0; b < total; b += full_chunk) sizes.push_back(std::min(full_chunk, total - b));
             return sizes;
         }
-        const int64_t ramp[2] = {full_chunk / 4, full_chunk / 2};
-        std::vector<int64_t> tail_sizes{ramp[1], ramp[0]};
-        int64_t left = total - (ramp[0] + ramp[1]) * 2;
-        sizes.push_back(ramp[0]);
-        sizes.push_back(ramp[1]);
+        // head ramp full/2^h .. full/2, tail ramp full/2 .. full/2^t
+        std::vector<int64_t> head, tail;
+        for (int j = ramp_head; j >= 1; --j) head.push_back(std::max<int64_t>(1024, full_chunk >> j));
+        for (int j = 1; j <= ramp_tail; ++j) tail.push_back(std::max<int64_t>(1024, full_chunk >> j));
+        int64_t left = total;
+        for (int64_t v : head) left -= v;
+        for (int64_t v : tail) left -= v;
+        if (left < 0) {  // too short for the ramps: uniform chunks
+            for (int64_t b = 0; b < total; b += full_chunk) sizes.push_back(std::min(full_chunk, total - b));
+            return sizes;
+        }
+        sizes = head;
         while (left > 0) {
             sizes.push_back(std::min(full_chunk, left));
             left -= sizes.back();
         }
-        sizes.insert(sizes.end(), tail_sizes.begin(), tail_sizes.end());
+        sizes.insert(sizes.end(), tail.begin(), tail.end());
         return sizes;
     };
 

@@ -443,13 +443,15 @@ def test_concurrent_callers_share_one_tree(oracle):
     assert not errors, errors
 
 
-@pytest.mark.parametrize("staging,streams,chunk_div,budget,first_div", [
-    ("1", "4", "8", "-1", "1"),     # defaults: full staging, graduated chunks
-    ("0", "4", "8", "-1", "1"),     # ring staging (slot reuse waits)
-    ("1", "2", "16", "40", "4"),    # forced overflow in every chunk, smaller first budget
-    ("0", "3", "5", "7", "1"),      # ring + forced overflow + resume
+@pytest.mark.parametrize("staging,streams,chunk_div,budget,first_div,ramp", [
+    ("1", "4", "8", "-1", "1", "2,2"),     # defaults: full staging, graduated chunks
+    ("0", "4", "8", "-1", "1", "2,2"),     # ring staging (slot reuse waits)
+    ("1", "2", "16", "40", "4", "2,2"),    # forced overflow in every chunk, smaller first budget
+    ("0", "3", "5", "7", "1", "2,2"),      # ring + forced overflow + resume
+    ("1", "4", "2", "-1", "1", "5,1"),     # deep head ramp, short tail ramp
+    ("0", "2", "2", "40", "1", "0,6"),     # no head ramp, deep tail ramp, ring staging
 ])
-def test_host_pipeline_chunks_exact(oracle, staging, streams, chunk_div, budget, first_div, monkeypatch):
+def test_host_pipeline_chunks_exact(oracle, staging, streams, chunk_div, budget, first_div, ramp, monkeypatch):
     """fkd_run_batch's chunked pipeline (capi.cu: copy-in stream, slot streams,
     high-priority tail stream, copy-out stream; full or ring staging) returns
     exactly the oracle's results and the device path's, with over-budget
@@ -461,8 +463,11 @@ def test_host_pipeline_chunks_exact(oracle, staging, streams, chunk_div, budget,
     monkeypatch.setenv("FKD_BUDGET", budget)
     monkeypatch.setenv("FKD_FIRST_BUDGET_DIV", first_div)
     monkeypatch.setenv("FKD_RESUME_MIN", "50")
+    monkeypatch.setenv("FKD_RAMP_HEAD", ramp.split(",")[0])
+    monkeypatch.setenv("FKD_RAMP_TAIL", ramp.split(",")[1])
     pts = fk.clustered_points(5, 1, 60_000, 3)
-    qs = fk.clustered_points(5, 2, 2_600_001, 3)[::5].copy()  # 520,001 queries: several 256k-capped chunks
+    # 650,001 queries: > 2 x the 256k minimum full chunk, so the graduated schedule (ramps) is used
+    qs = fk.clustered_points(5, 2, 2_600_001, 3)[::4].copy()
     nodes = oracle.build_tree(pts)
     tree = fk.KdTree.from_level_order(nodes)
     for kind, k, r in ((fk.QueryKind.fcp, 1, INF), (fk.QueryKind.knn, 8, INF), (fk.QueryKind.knn, 20, 0.01)):
