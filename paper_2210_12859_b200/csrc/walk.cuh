@@ -269,6 +269,15 @@ __device__ __forceinline__ int dim_down(int d) {  // split dim one level up
 #define FKD_SLOT_LIST_MIN_D 8
 #endif
 
+// Lists of >= FKD_STREAM_IO_MIN_KB slots read their query and write their
+// final results with the evict-first (.cs) cache hint, so the streamed query /
+// result lines (kNN8: 76 B per query) displace fewer tree lines in L2.
+// Measured (tools/stream_io_ab.sh, profiles/r01j_stream_io_ab.log): kNN8 walk
+// -0.4% clustered and uniform, fcp +0.3% (so fcp keeps the plain path).
+#ifndef FKD_STREAM_IO_MIN_KB
+#define FKD_STREAM_IO_MIN_KB 8
+#endif
+
 template <int D, int S, int KB, bool STATS, bool UNORDERED>
 struct LaneWalk {
     // With a split-plane slot in the store (S > D) the walk never needs the
@@ -276,6 +285,7 @@ struct LaneWalk {
     // coordinate split at the current depth (rotated by one per level).
     static constexpr bool kRot = S > D && D > 1;
     static constexpr int kKB = KB;
+    static constexpr bool kStreamIO = KB >= FKD_STREAM_IO_MIN_KB;
     static constexpr int kD = D;
     // Slot-list mode (high dimensions, 16 slots): the sorted list lives in the
     // query's own output slot (Hit format, k entries) and only its kth key is
@@ -295,12 +305,18 @@ struct LaneWalk {
     // Loads the query and resets the state (traverse.hpp:250-255).  Returns
     // false (and flags the id) for a non-finite query (batch.cpp:79).
     __device__ __forceinline__ bool init(const WalkArgs& a, int64_t pos) {
-        qi = a.order ? int64_t(__ldg(a.order + pos)) : pos;
+        if constexpr (kStreamIO)
+            qi = a.order ? int64_t(__ldcs(a.order + pos)) : pos;
+        else
+            qi = a.order ? int64_t(__ldg(a.order + pos)) : pos;
         const float* qp = a.queries + qi * D;
         bool finite = true;
 #pragma unroll
         for (int j = 0; j < D; ++j) {
-            q[j] = __ldg(qp + j);
+            if constexpr (kStreamIO)
+                q[j] = __ldcs(qp + j);
+            else
+                q[j] = __ldg(qp + j);
             finite &= isfinite(q[j]);
         }
         if (!finite) {
@@ -535,13 +551,22 @@ struct LaneWalk {
                 if (s >= 0) {
                     const uint64_t key = L[j];
                     const bool hit = uint32_t(key) != 0xFFFFFFFFu;  // empty slot -> Hit{-1, +inf}
-                    out[s] = make_int2(int32_t(uint32_t(key)),
-                                       hit ? int32_t(uint32_t(key >> 32) - 1u) : 0x7f800000);
+                    const int2 h = make_int2(int32_t(uint32_t(key)),
+                                             hit ? int32_t(uint32_t(key >> 32) - 1u) : 0x7f800000);
+                    if (kStreamIO && final)
+                        __stcs(out + s, h);
+                    else
+                        out[s] = h;
                     c += hit;
                 }
             }
         }
-        if (final) a.counts[qi] = c;
+        if (final) {
+            if (kStreamIO)
+                __stcs(a.counts + qi, c);
+            else
+                a.counts[qi] = c;
+        }
         if constexpr (STATS) {
             if (a.per_query) {
                 unsigned long long s = cnt.steps, v = cnt.visited;
