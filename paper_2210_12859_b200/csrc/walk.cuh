@@ -274,6 +274,9 @@ __device__ __forceinline__ int dim_down(int d) {  // split dim one level up
 // result lines (kNN8: 76 B per query) displace fewer tree lines in L2.
 // Measured (tools/stream_io_ab.sh, profiles/r01j_stream_io_ab.log): kNN8 walk
 // -0.4% clustered and uniform, fcp +0.3% (so fcp keeps the plain path).
+#ifndef FKD_STREAM_QUERY_LOADS
+#define FKD_STREAM_QUERY_LOADS 1
+#endif
 #ifndef FKD_STREAM_IO_MIN_KB
 #define FKD_STREAM_IO_MIN_KB 8
 #endif
@@ -313,7 +316,7 @@ struct LaneWalk {
         bool finite = true;
 #pragma unroll
         for (int j = 0; j < D; ++j) {
-            if constexpr (kStreamIO)
+            if constexpr (kStreamIO && FKD_STREAM_QUERY_LOADS)
                 q[j] = __ldcs(qp + j);
             else
                 q[j] = __ldg(qp + j);
