@@ -265,6 +265,12 @@ __device__ __forceinline__ int dim_down(int d) {  // split dim one level up
 
 // Lowest dimension whose 16-slot walks keep the list in the output slot
 // (LaneWalk::kSlot); 9 turns the mode off.
+// Experiment knob: kNN lists compute the distance only on a first visit
+// (a divergent block, as fcp in D != 3) instead of every trip.
+#ifndef FKD_KNN_DIST_BRANCH
+#define FKD_KNN_DIST_BRANCH 0
+#endif
+
 #ifndef FKD_SLOT_LIST_MIN_D
 #define FKD_SLOT_LIST_MIN_D 8
 #endif
@@ -368,7 +374,7 @@ struct LaneWalk {
             load_point<D, S>(a.nodes, curr, p);
             pd = pick(p, d);
         }
-        if constexpr (KB > 1 || D == 3) {
+        if constexpr ((KB > 1 && !FKD_KNN_DIST_BRANCH) || (KB == 1 && D == 3)) {
             // traverse.hpp:217-222.  kNN, and 3-D fcp: the distance is
             // computed every trip (no divergent block; measured faster: fcp
             // 3-D -3.6% with the packed-pair distance, but 4-D +22%, and the
@@ -386,9 +392,14 @@ struct LaneWalk {
                 r2 = key_dist(L[KB - 1]);
             }
         } else if (from_parent) {  // fcp, D != 3: a branch is cheaper than the FP ops
-            const float d2 = sq_dist<D, (D <= 4)>(q, p);
+            const float d2 = sq_dist<D, (D <= 4 && KB <= 8)>(q, p);
             const uint64_t key = make_key(d2, curr);
-            if (key_lt(key, L[KB - 1])) {  // d2 <= cap2 and beats the best (cap_key)
+            if constexpr (kSlot) {
+                if (key_lt(key, L[0])) {
+                    slot_insert(a, key);
+                    r2 = key_dist(L[0]);
+                }
+            } else if (key_lt(key, L[KB - 1])) {  // d2 <= cap2 and beats the kth (cap_key)
                 list_insert(L, key);
                 r2 = key_dist(L[KB - 1]);
             }
