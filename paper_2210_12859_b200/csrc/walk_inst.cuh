@@ -28,13 +28,26 @@ void launch_overflow(const WalkArgs& a, cudaStream_t st) {
     overflow_kernel<D, S, KB, T><<<sms * per_sm, T, 0, st>>>(a);
 }
 
+// Experiment knob FKD_L1_CARVEOUT=<percent>: preferred shared-memory carveout
+// of the (shared-memory-free) walk kernels; unset leaves the driver's choice.
+template <class K>
+void set_carveout(K kernel) {
+    static const int pct = [] {
+        const char* e = std::getenv("FKD_L1_CARVEOUT");
+        return e ? std::max(0, std::min(100, std::atoi(e))) : -1;
+    }();
+    if (pct >= 0) cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+}
+
 template <int D, int S, int KB, bool STATS, bool UNORDERED>
 void launch_one(const WalkArgs& a, cudaStream_t st) {
+    set_carveout(walk_kernel<D, S, KB, STATS, UNORDERED>);
     walk_kernel<D, S, KB, STATS, UNORDERED><<<walk_blocks(a.m, kWalkThreads), kWalkThreads, 0, st>>>(a);
 }
 
 template <int D, int S, int KB, bool UNORDERED>
 void launch_round(const WalkArgs& a, cudaStream_t st) {
+    set_carveout(walk_round_kernel<D, S, KB, UNORDERED>);
     walk_round_kernel<D, S, KB, UNORDERED><<<walk_blocks(a.m, kWalkThreads), kWalkThreads, 0, st>>>(a);
 }
 
