@@ -204,14 +204,15 @@ cudaError_t grow(T*& p, int64_t& cap, int64_t need) {
 
 struct Replica {
     int device = 0;
-    float* nodes = nullptr;  // n x stride
+    float* alloc = nullptr;  // node_shift() + n slots of stride floats
+    float* nodes = nullptr;  // alloc + node_shift() * stride: node i's slot
     std::mutex mu;
     std::vector<Workspace*> pool;
 
     ~Replica() {
         for (Workspace* w : pool) delete w;
         cudaSetDevice(device);
-        cudaFree(nodes);
+        cudaFree(alloc);
     }
 };
 
@@ -687,6 +688,28 @@ static fkd_status set_frame(fkd_tree* t, const float* lo, const float* hi) {
     return FKD_OK;
 }
 
+// The store starts node_shift() empty slots into its allocation.  With one
+// slot, siblings 2c+1 / 2c+2 share an aligned pair of slots (for 16-byte
+// nodes: one 32-byte sector) instead of straddling two, so the far child's
+// sector usually arrived with the close child's.  Measured
+// (tools/node_shift_ab.sh, profiles/r01j_node_shift_ab.log): C3 kNN8 walk
+// -1.6%, fcp -1.5%, uniform kNN8 -0.8%, 4-D kNN16 -1%; FKD_NODE_SHIFT=0
+// restores the unshifted store.
+static int64_t node_shift() {
+    static const int64_t v = [] {
+        const char* e = std::getenv("FKD_NODE_SHIFT");
+        return e ? int64_t(std::max(0, std::min(8, std::atoi(e)))) : int64_t(1);
+    }();
+    return v;
+}
+
+static fkd_status alloc_store(Replica* r, int64_t n, int stride) {
+    const int64_t sh = node_shift();
+    FKD_CUDA(cudaMalloc(&r->alloc, size_t(n + sh) * stride * sizeof(float)));
+    r->nodes = r->alloc + sh * stride;
+    return FKD_OK;
+}
+
 static fkd_status make_replica(fkd_tree* t, int dev, const float* src, bool src_on_device,
                                cudaStream_t st) {
     auto* r = new Replica();
@@ -696,7 +719,7 @@ static fkd_status make_replica(fkd_tree* t, int dev, const float* src, bool src_
     const int64_t n = t->n;
     if (n == 0) return FKD_OK;
     const size_t store_bytes = size_t(n) * t->stride * sizeof(float);
-    FKD_CUDA(cudaMalloc(&r->nodes, store_bytes));
+    if (fkd_status e = alloc_store(r, n, t->stride); e != FKD_OK) return e;
     if (t->stride == t->dim) {
         FKD_CUDA(cudaMemcpyAsync(r->nodes, src, store_bytes,
                                  src_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
@@ -732,7 +755,7 @@ static fkd_status peer_replica(fkd_tree* t, int dev) {
     if (t->n == 0) return FKD_OK;
     const size_t bytes = size_t(t->n) * t->stride * sizeof(float);
     DeviceGuard g(dev);
-    FKD_CUDA(cudaMalloc(&r->nodes, bytes));
+    if (fkd_status e = alloc_store(r, t->n, t->stride); e != FKD_OK) return e;
     if (dev == src->device) {
         FKD_CUDA(cudaMemcpy(r->nodes, src->nodes, bytes, cudaMemcpyDeviceToDevice));
     } else {
