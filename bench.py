@@ -16,7 +16,10 @@ replicated with an NCCL broadcast; every rank walks its own M queries
 
 ``--impl reference`` times the reference's own ``flatkd::run_batch``
 (oracle/_ref, compiled unmodified from the reference sources) with all
-host threads on a bounded sample of the same workload.
+host threads over the same full batches (C5's 1B queries: a 10M sample),
+generating the identical inputs with the reference's own RNG; it never
+loads the product library.  ``e2e_pageable`` times the drop-in with
+NumPy (pageable) buffers, the way a reference caller's std::vectors arrive.
 """
 from __future__ import annotations
 
@@ -53,10 +56,61 @@ SEED = 1
 METRIC = "fcp & kNN(k=8) queries/sec, 3D float, N=10M, 1/2/4/8 B200 vs host CPU"
 
 
-def gen_points(fk, kind: str, stream: int, count: int, dim: int) -> np.ndarray:
+def gen_points(gen, kind: str, stream: int, count: int, dim: int) -> np.ndarray:
+    """Workload points from `gen`: the product's host generators (B200 arm)
+    or the reference library's (reference arm, oracle/ref_capi.cpp) — the
+    two are byte-identical (tests/test_host.py), so both arms walk the same
+    inputs while the reference arm never loads the product library."""
     if kind == "clustered":
-        return fk.clustered_points(SEED, stream, count, dim, 64, 0.02)
-    return fk.random_points(SEED, stream, count, dim)
+        return gen.clustered_points(SEED, stream, count, dim, 64, 0.02)
+    if hasattr(gen, "stream_points"):
+        return gen.stream_points(SEED, stream, count, dim)
+    return gen.random_points(SEED, stream, count, dim)
+
+
+def query_stream(rank: int) -> int:
+    """RNG stream of a rank's queries (weak scaling): rank 0 uses the
+    reference's query stream (rng.hpp:24), other ranks private streams
+    (same rule as paper_2210_12859_b200.shard.query_stream)."""
+    return 2 if rank == 0 else 1000 + rank
+
+
+def workload_config(workload: str, world: int) -> dict:
+    """The `config` object of the JSON line — identical in both arms."""
+    desc, n, m, dim, gkind, batches = WORKLOADS[workload]
+    strong = workload == "c5"
+    return {"workload": desc, "tree_n": n, "queries_per_gpu": (m // world if strong else m), "dim": dim,
+            "batches_per_step": [("fcp" if kk == "fcp" else f"knn{k2}") for kk, k2, _ in batches],
+            "max_radius": [rr for _, _, rr in batches], "parallelism": f"query-sharded x{world}",
+            "l2": "flushed: the B200 arm writes a 256 MB buffer (> 126 MB L2) between timed steps "
+                  f"(untimed); inputs {m * dim * 4 / 1e6:.0f} MB of queries + {n * 16 / 1e6:.0f} MB tree store",
+            "morton": True, "seed": SEED}
+
+
+def host_cpu() -> dict:
+    """Host cores and CPU model of this box (BASELINE.md §3 asks for both)."""
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count() or 1, "cpu_model": model}
+
+
+def repo_native_libs() -> list:
+    """In-repo shared libraries mapped into this process (which native code ran)."""
+    libs = set()
+    try:
+        for line in open("/proc/self/maps"):
+            path = line.split()[-1] if len(line.split()) >= 6 else ""
+            if path.endswith(".so") and path.startswith(ROOT):
+                libs.add(os.path.relpath(path, ROOT))
+    except OSError:
+        pass
+    return sorted(libs)
 
 
 def bytes_per_query(dim: int, p_bar: float, stride: int) -> float:
@@ -143,53 +197,61 @@ def dist_env():
 # ----------------------------------------------------------------------------- reference arm
 
 def run_reference(args) -> None:
+    """The reference's own flatkd::run_batch (oracle/_ref, built unmodified
+    from /root/reference by oracle/Makefile) over the FULL batch of every
+    step, timed exactly as run_cell does (bench.cpp:35-41: run_batch only).
+    Nothing from the product package is imported or loaded here."""
     world, rank, _ = dist_env()
     if rank != 0:
         return
-    import paper_2210_12859_b200 as fk  # generators only (input data, not the path)
     from oracle import Reference
-    from paper_2210_12859_b200.shard import query_stream
 
     desc, n, m, dim, gkind, batches = WORKLOADS[args.workload]
     ref = Reference()
     threads = ref.hardware_threads()
-    pts = gen_points(fk, gkind, 1, n, dim)
-    # the tree is input, not the path: flatkd::build_tree (untimed, as bench.cpp
-    # does); above 20M points its single-threaded build takes minutes (155 s at
-    # 100M), so the byte-identical multi-threaded host builder stands in
-    nodes = ref.build_tree(pts) if n <= 20_000_000 else fk.build_level_order(pts)
-    sample = min(m, args.ref_sample)
-    qs = gen_points(fk, gkind, query_stream(0), m, dim)[:sample]
-    times = []
+    # the tree is input, not the path: flatkd::build_tree, untimed (bench.hpp:35-37)
+    nodes = ref.build_tree(gen_points(ref, gkind, 1, n, dim))
+    strong = args.workload == "c5"
+    m_rank = m // world if strong else m
+    sample = m_rank if args.ref_sample <= 0 else min(m_rank, args.ref_sample)
+    qs = gen_points(ref, gkind, 2 if strong else query_stream(0), sample, dim)
+    times, hashes = [], {}
     for it in range(args.warmup + args.steps):
         t = 0.0
         for kind, k, r in batches:
-            _, _, _, secs = ref.run_batch(nodes, qs, kind, k, r, threads=0)
+            c, h, _, secs = ref.run_batch(nodes, qs, kind, k, r, threads=0)
             t += secs
+            if it == 0:
+                hashes[kind if kind == "fcp" else f"knn{k}"] = f"{ref.result_hash(c, h, k if kind == 'knn' else 1):016x}"
         if it >= args.warmup:
             times.append(t)
     step = float(np.mean(times))
     value = len(batches) * sample / step
+    cpu = host_cpu()
+    what = "every query of the batch" if sample == m_rank else f"first {sample} of the {m_rank} queries"
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": step * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic",
-        "config": {"workload": desc, "sample_queries_per_batch": sample, "tree_n": n,
-                   "batches": [f"{k_}{'' if k_ == 'fcp' else kk}" for k_, kk, _ in batches]},
+        "higher_is_better": True, "scaling": "strong" if strong else "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic", "config": workload_config(args.workload, world),
         "cpu_baseline": {"value": value, "unit": "queries/s", "cores": threads, "kind": "reference",
-                         "sample": f"first {sample} of the {m} queries, each batch of the step, "
-                                   "flatkd::run_batch (Engine::stack_free, OpenMP all threads)"},
+                         **cpu, "sample": f"{what}, each batch of the step, flatkd::run_batch "
+                                          "(Engine::stack_free, OpenMP, all host threads), rank 0 only"},
         "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "result_hash": hashes,
+        "native_libs": repo_native_libs(),
     }
+    assert not any("libfkd_b200" in x for x in line["native_libs"]), "reference arm loaded the product"
     print(json.dumps(line), flush=True)
 
 
 # ----------------------------------------------------------------------------- B200 arm
 
-def cpu_baseline_leg(fk, nodes, qs_host, batches, sample, gpu_tree) -> dict:
-    """The reference run_batch on the host cores, same tree/queries (sample),
-    plus a parity check of the GPU results on that sample."""
+def cpu_baseline_leg(nodes, qs_host, batches, sample, gpu_hashes) -> dict:
+    """The reference's run_batch on this box's host cores over the same tree
+    and queries (the whole batch unless --cpu-sample caps it), timed as
+    run_cell does (bench.cpp:35-41), plus its result hashes against the
+    B200 path's (the device-resident outputs of the timed steps)."""
     from oracle import REF_SO, Oracle, Reference
 
     kind_name = "reference" if os.path.exists(REF_SO) else "port"
@@ -200,28 +262,34 @@ def cpu_baseline_leg(fk, nodes, qs_host, batches, sample, gpu_tree) -> dict:
     for kind, k, r in batches:
         if kind_name == "reference":
             c, h, _, secs = impl.run_batch(nodes, q, kind, k, r, threads=0)
-            ref_hash = impl.result_hash(c, h, k if kind == "knn" else 1)
         else:
             t0 = time.perf_counter()
             c, h, _, _ = impl.run_batch(nodes, q, kind, k, r, threads=0)
             secs = time.perf_counter() - t0
-            ref_hash = impl.result_hash(c, h, k if kind == "knn" else 1)
         total_t += secs
-        res = fk.run_batch(gpu_tree, q, fk.BatchOptions(kind=fk.QueryKind[kind], k=k, max_radius=r))
-        parity &= res.result_hash() == ref_hash
-    cores = os.cpu_count() or 1
-    return {"value": len(batches) * sample / total_t, "unit": "queries/s", "cores": cores,
-            "kind": kind_name, "parity_hash_equal": bool(parity),
-            "sample": f"first {sample} queries of rank 0, every batch of the step, "
+        name = kind if kind == "fcp" else f"knn{k}"
+        if sample == len(qs_host):
+            parity &= f"{impl.result_hash(c, h, k if kind == 'knn' else 1):016x}" == gpu_hashes[name]
+    cpu = host_cpu()
+    threads = impl.hardware_threads() if kind_name == "reference" else cpu["nproc"]
+    what = "every query of rank 0's batch" if sample == len(qs_host) else f"first {sample} queries of rank 0"
+    line = {"value": len(batches) * sample / total_t, "unit": "queries/s", "cores": threads,
+            "kind": kind_name, **cpu,
+            "sample": f"{what}, every batch of the step, "
                       f"{'flatkd::run_batch from oracle/_ref' if kind_name == 'reference' else 'oracle port'}"
-                      f" with {cores} OpenMP threads"}
+                      f" with {threads} OpenMP threads"}
+    if sample == len(qs_host):
+        line["parity_hash_equal"] = bool(parity)
+    return line
 
 
 def run_b200(args) -> None:
+    import ctypes as C
+
     import torch
 
     import paper_2210_12859_b200 as fk
-    from paper_2210_12859_b200.shard import max_over_ranks, query_stream, replicate_tree
+    from paper_2210_12859_b200.shard import max_over_ranks, replicate_tree, shard_range
 
     world, rank, local = dist_env()
     dist = None
@@ -235,8 +303,8 @@ def run_b200(args) -> None:
     dev = torch.device("cuda", torch.cuda.current_device())
     desc, n, m, dim, gkind, batches = WORKLOADS[args.workload]
 
-    # ---- tree: built on rank 0, replicated by NCCL broadcast
-    # GPU build on rank 0 (csrc/build.cu, byte-identical to flatkd::build_tree)
+    # ---- tree: built on rank 0 (GPU builder, byte-identical to
+    # flatkd::build_tree), replicated by NCCL broadcast
     if rank == 0:
         nodes_dev = fk.build_level_order_device(torch.from_numpy(gen_points(fk, gkind, 1, n, dim)).to(dev))
         nodes_host = nodes_dev.cpu().numpy()
@@ -248,8 +316,6 @@ def run_b200(args) -> None:
 
     strong = args.workload == "c5"
     if strong:  # 1B queries split across the ranks (contiguous blocks of one stream)
-        from paper_2210_12859_b200.shard import shard_range
-
         lo, hi = shard_range(m, world, rank)
         m = hi - lo
         qs_host = gen_points(fk, gkind, 2, hi, dim)[lo:hi].copy() if world > 1 else gen_points(fk, gkind, 2, m, dim)
@@ -308,51 +374,78 @@ def run_b200(args) -> None:
     t_step = max_over_ranks(sum(step_ms), dev) / args.steps / 1e3  # seconds, max over ranks
     m_total = WORKLOADS[args.workload][2] if strong else world * m
     value = len(batches) * m_total / t_step
-
-    # ---- e2e through the host-buffer C ABI (pinned buffers), same metric
-    import ctypes as C
-
-    hq = fk.LIB.fkd_host_alloc(qs_host.nbytes)
-    C.memmove(hq, qs_host.ctypes.data, qs_host.nbytes)
-    host_out = {}
+    gpu_hashes = {}
     for kind, k, _ in batches:
-        host_out[(kind, k)] = (fk.LIB.fkd_host_alloc(m * 4), fk.LIB.fkd_host_alloc(m * k * 8))
+        c, h = outs[(kind, k)]
+        gpu_hashes[kind if kind == "fcp" else f"knn{k}"] = \
+            f"{fk.result_hash(c.cpu().numpy(), h.cpu().numpy().view(fk.HIT_DTYPE), k):016x}"
+
+    # ---- e2e through the host-buffer C ABI, same metric: H2D of the step's
+    # queries, the walk and D2H of every result slot inside the timed region.
+    # Pinned caller buffers (fkd_host_alloc) -> `e2e`; the drop-in as a
+    # reference caller makes it (NumPy / std::vector, pageable) -> `e2e_pageable`.
     h2d = d2h = 0
     for kind, k, _ in batches:
         h2d += m * dim * 4
         d2h += m * 4 + m * k * 8
 
-    def e2e_step():
-        for (kind, k, _), o in zip(batches, opts):
-            hc, hh = host_out[(kind, k)]
-            co = o.to_c()
-            rc = fk.LIB.fkd_run_batch(tree.handle, hq, m, dim, C.byref(co), hc, hh, None)
-            if rc != 0:
-                raise RuntimeError(fk.LIB.fkd_last_error().decode())
+    def host_buffers(pinned: bool):
+        bufs = {}
+        if pinned:
+            hq = fk.LIB.fkd_host_alloc(qs_host.nbytes)
+            C.memmove(hq, qs_host.ctypes.data, qs_host.nbytes)
+            for kind, k, _ in batches:
+                bufs[(kind, k)] = (fk.LIB.fkd_host_alloc(m * 4), fk.LIB.fkd_host_alloc(m * k * 8))
+            return hq, bufs
+        keep = [qs_host]
+        for kind, k, _ in batches:
+            c_arr, h_arr = np.empty(m, np.int32), np.empty(m * k, np.int64)
+            c_arr.fill(0)  # pages touched, as a reference BatchResult's are (batch.cpp:82-86)
+            h_arr.fill(-1)
+            keep += [c_arr, h_arr]
+            bufs[(kind, k)] = (c_arr.ctypes.data, h_arr.ctypes.data)
+        bufs["keep"] = keep
+        return qs_host.ctypes.data, bufs
 
-    for _ in range(max(1, args.warmup)):
-        e2e_step()
-    if dist is not None:
-        dist.barrier()
-    e2e_times = []
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        e2e_step()
-        e2e_times.append(time.perf_counter() - t0)
-    e2e_value = len(batches) * m_total / (max_over_ranks(sum(e2e_times), dev) / args.steps)
-    # results of the e2e path must equal the device path (same queries)
-    e2e_parity = True
-    for kind, k, _ in batches:
-        hc, hh = host_out[(kind, k)]
-        c, h = outs[(kind, k)]
-        got_c = np.ctypeslib.as_array(C.cast(hc, C.POINTER(C.c_int32)), shape=(m,))
-        got_h = np.ctypeslib.as_array(C.cast(hh, C.POINTER(C.c_int64)), shape=(m * k,))
-        e2e_parity &= bool(np.array_equal(got_c, c.cpu().numpy()))
-        e2e_parity &= bool(np.array_equal(got_h, h.view(torch.int64).cpu().numpy()))
-    for hc, hh in host_out.values():
-        fk.LIB.fkd_host_free(hc)
-        fk.LIB.fkd_host_free(hh)
-    fk.LIB.fkd_host_free(hq)
+    def e2e_run(pinned: bool) -> tuple[float, bool]:
+        hq, bufs = host_buffers(pinned)
+
+        def e2e_step():
+            for (kind, k, _), o in zip(batches, opts):
+                hc, hh = bufs[(kind, k)]
+                co = o.to_c()
+                rc = fk.LIB.fkd_run_batch(tree.handle, hq, m, dim, C.byref(co), hc, hh, None)
+                if rc != 0:
+                    raise RuntimeError(fk.LIB.fkd_last_error().decode())
+
+        for _ in range(max(1, args.warmup)):
+            e2e_step()
+        if dist is not None:
+            dist.barrier()
+        times = []
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            e2e_step()
+            times.append(time.perf_counter() - t0)
+        val = len(batches) * m_total / (max_over_ranks(sum(times), dev) / args.steps)
+        # results of the e2e path must equal the device path (same queries)
+        same = True
+        for kind, k, _ in batches:
+            hc, hh = bufs[(kind, k)]
+            c, h = outs[(kind, k)]
+            got_c = np.ctypeslib.as_array(C.cast(hc, C.POINTER(C.c_int32)), shape=(m,))
+            got_h = np.ctypeslib.as_array(C.cast(hh, C.POINTER(C.c_int64)), shape=(m * k,))
+            same &= bool(np.array_equal(got_c, c.cpu().numpy()))
+            same &= bool(np.array_equal(got_h, h.view(torch.int64).cpu().numpy()))
+        if pinned:
+            for key, (hc, hh) in bufs.items():
+                fk.LIB.fkd_host_free(hc)
+                fk.LIB.fkd_host_free(hh)
+            fk.LIB.fkd_host_free(hq)
+        return val, same
+
+    e2e_value, e2e_parity = e2e_run(True)
+    e2e_pg_value, e2e_pg_parity = e2e_run(False) if not args.no_pageable else (None, None)
 
     if rank != 0:
         if dist is not None:
@@ -373,26 +466,24 @@ def run_b200(args) -> None:
     for b, (kk, k2, r2) in enumerate(batches):
         name = kk if kk == "fcp" else f"knn{k2}"
         tw = float(np.mean(walk_ms[b])) / 1e3
+        bpq = bytes_per_query(dim, pbar[(kk, k2)], k2 if kk == "knn" else 1)
         per_batch[name] = {"walk_ms": tw * 1e3, "walk_qps": m / tw, "P_bar": pbar[(kk, k2)],
-                           "bytes_per_query": bytes_per_query(dim, pbar[(kk, k2)], k2 if kk == "knn" else 1),
-                           "hbm_frac": m * bytes_per_query(dim, pbar[(kk, k2)], k2 if kk == "knn" else 1) / tw / 1e9 / peak}
+                           "bytes_per_query": bpq, "hbm_frac": m * bpq / tw / 1e9 / peak,
+                           "result_hash": gpu_hashes[name]}
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline_leg(fk, nodes_host, qs_host, batches, min(m, args.cpu_sample), tree)
+        sample = m if args.cpu_sample <= 0 else min(m, args.cpu_sample)
+        cpu = cpu_baseline_leg(nodes_host, qs_host, batches, sample, gpu_hashes)
 
     line = {
         "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True,
         "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": desc, "tree_n": n, "queries_per_gpu": m, "dim": dim,
-                   "batches_per_step": [("fcp" if kk == "fcp" else f"knn{k2}") for kk, k2, _ in batches],
-                   "max_radius": [rr for _, _, rr in batches], "parallelism": f"query-sharded x{world}",
-                   "l2": "256 MB buffer written between timed steps (untimed); inputs 120+160 MB > L2",
-                   "morton": True},
+        "config": workload_config(args.workload, world),
         "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "results_equal_device_path": bool(e2e_parity),
-                "path": "fkd_run_batch (C ABI, pinned host buffers, chunked H2D/walk/D2H)"},
+                "path": "fkd_run_batch (C ABI, pinned host buffers from fkd_host_alloc, chunked H2D/walk/D2H)"},
         "gpu_launches": launches // args.steps,
         "gpu_launches_note": "own kernels per timed step (per batch: Morton keys, walk, continuation "
                              "rounds (fcp: 3), resume pass, CTA overflow pass); CUB sort kernels excluded",
@@ -410,7 +501,13 @@ def run_b200(args) -> None:
             "source": "instruction count per launch from profiles/traffic.json (ncu), time live"},
         "per_batch": per_batch,
         "clocks": sampler.summary(),
+        "native_libs": repo_native_libs(),
     }
+    if e2e_pg_value is not None:
+        line["e2e_pageable"] = {"value": e2e_pg_value, "unit": "queries/s", "h2d_bytes_per_step": h2d,
+                                "d2h_bytes_per_step": d2h, "results_equal_device_path": bool(e2e_pg_parity),
+                                "path": "fkd_run_batch with NumPy (pageable) buffers, as flatkd::b200::run_batch "
+                                        "passes a reference BatchResult's std::vectors"}
     if line.get("issue_roofline"):
         line["issue_roofline"]["frac"] = line["issue_roofline"]["achieved"] / line["issue_roofline"]["peak"]
     if cpu is not None:
@@ -427,12 +524,20 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c3")
-    ap.add_argument("--cpu-sample", type=int, default=1_000_000)
-    ap.add_argument("--ref-sample", type=int, default=1_000_000)
+    ap.add_argument("--cpu-sample", type=int, default=-1,
+                    help="queries of the cpu_baseline leg (<=0: the whole batch; default: whole "
+                         "batch up to 20M queries, else 10M)")
+    ap.add_argument("--ref-sample", type=int, default=-1,
+                    help="queries per batch of the reference arm (same rule as --cpu-sample)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-pageable", action="store_true", help="skip the e2e_pageable measurement")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    m_rank = WORKLOADS[args.workload][2] // (int(os.environ.get("WORLD_SIZE", "1")) if args.workload == "c5" else 1)
+    for attr in ("cpu_sample", "ref_sample"):  # whole batch where the host finishes it in seconds
+        if getattr(args, attr) < 0:
+            setattr(args, attr, 0 if m_rank <= 20_000_000 else 10_000_000)
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -252,6 +252,12 @@ class Reference:
         L.fkr_read_file.argtypes = [C.c_char_p, C.c_int, _f32p, C.c_longlong, C.POINTER(C.c_longlong),
                                     C.POINTER(C.c_int)]
         L.fkr_layout.argtypes = [C.POINTER(C.c_int)]
+        L.fkr_clustered_points.argtypes = [C.c_uint64, C.c_uint64, C.c_longlong, C.c_int, C.c_int,
+                                           C.c_float, _f32p]
+        L.fkr_bench_matrix_csv.restype = C.c_longlong
+        L.fkr_bench_matrix_csv.argtypes = [C.c_longlong, C.c_int, C.c_int, C.c_int, C.c_int,
+                                           C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_void_p,
+                                           C.c_int, C.c_char_p, C.c_longlong]
 
     def _check(self, rc: int):
         if rc != 0:
@@ -287,6 +293,32 @@ class Reference:
 
     def derive_stream_seed(self, master: int, stream: int) -> int:
         return self.lib.fkr_derive_stream_seed(master, stream)
+
+    def stream_points(self, master: int, stream: int, count: int, dim: int) -> np.ndarray:
+        """random_points(derive_stream_seed(master, stream), count, dim) (rng.hpp:26-53)."""
+        return self.random_points(self.derive_stream_seed(master, stream), count, dim)
+
+    def clustered_points(self, master: int, stream: int, count: int, dim: int, blobs: int = 64,
+                         sigma: float = 0.02) -> np.ndarray:
+        """The C3 Gaussian-blob workload on the reference's RNG (ref_capi.cpp)."""
+        out = np.empty(max(count * dim, 1), np.float32)
+        self._check(self.lib.fkr_clustered_points(master, stream, count, dim, blobs, sigma, out))
+        return out[: count * dim].reshape(count, dim)
+
+    def bench_matrix_csv(self, n_queries: int, k_dim: int, kind: str, reps: int, n_list,
+                         k_list=(8,), r_list=(float("inf"),), threads: int = 0) -> str:
+        """flatkd::run_bench_matrix + write_bench_csv (bench.cpp:64-133), seed 1."""
+        n_arr = (C.c_longlong * len(n_list))(*n_list)
+        k_arr = (C.c_int * len(k_list))(*k_list)
+        r_arr = (C.c_float * len(r_list))(*r_list)
+        args = (n_queries, k_dim, int(kind == "knn"), reps, threads, n_arr, len(n_list), k_arr,
+                len(k_list), r_arr, len(r_list))
+        size = self.lib.fkr_bench_matrix_csv(*args, None, 0)
+        if size < 0:
+            raise OracleError(9, self.last_error())
+        buf = C.create_string_buffer(size + 1)
+        self.lib.fkr_bench_matrix_csv(*args, buf, size + 1)
+        return buf.value.decode()
 
     def build_tree(self, points: np.ndarray) -> np.ndarray:
         pts = np.ascontiguousarray(points, np.float32)

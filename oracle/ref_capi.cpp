@@ -13,6 +13,7 @@
 //   testing::random_point_set/query src/testing/instancegen.cpp:12-48
 //   testing::run_*_suite            src/testing/selfcheck.cpp:94-266
 #include <chrono>
+#include <cmath>
 #include <cstddef>
 #include <cstdint>
 #include <cstring>
@@ -23,6 +24,7 @@
 #include <vector>
 
 #include "flatkd/batch.hpp"
+#include "flatkd/bench.hpp"
 #include "flatkd/error.hpp"
 #include "flatkd/io.hpp"
 #include "flatkd/rng.hpp"
@@ -88,6 +90,60 @@ int fkr_random_points(uint64_t seed, long long count, int dim, float* out) {
         auto p = flatkd::random_points(seed, count, dim);
         std::memcpy(out, p.raw().data(), p.raw().size() * sizeof(float));
     });
+}
+
+// The clustered C3 workload (no reference counterpart): the
+// same generator as the product's fkd_clustered_points, written here on the
+// reference's own RNG primitives (flatkd::random_points for the centres,
+// UniformFloatSource::next_u64 for blobs and Box-Muller draws, rng.hpp:33-53)
+// so the reference arm of bench.py needs nothing from the product library.
+int fkr_clustered_points(uint64_t master, uint64_t stream, long long count, int dim, int blobs,
+                         float sigma, float* out) {
+    return guarded([&] {
+        if (count < 0 || dim < 1 || blobs < 1) throw flatkd::DataError("clustered points: bad shape");
+        const flatkd::PointSet centres =
+            flatkd::random_points(flatkd::derive_stream_seed(master, 3), blobs, dim);
+        flatkd::UniformFloatSource src(flatkd::derive_stream_seed(master, stream));
+        const double two_pi = 6.283185307179586476925286766559;
+        for (long long i = 0; i < count; ++i) {
+            const std::uint64_t b = src.next_u64() % std::uint64_t(blobs);
+            for (int d = 0; d < dim; ++d) {
+                const double u1 = double(src.next_u64() >> 11) * 0x1p-53;
+                const double u2 = double(src.next_u64() >> 11) * 0x1p-53;
+                const double z = std::sqrt(-2.0 * std::log(1.0 - u1)) * std::cos(two_pi * u2);
+                out[i * dim + d] = centres.raw()[std::size_t(b) * dim + d] + static_cast<float>(z) * sigma;
+            }
+        }
+    });
+}
+
+// flatkd::run_bench_matrix (bench.cpp:64-90) + write_bench_csv (bench.cpp:119-133):
+// the reference's own Table-1 rows, CSV text into `out` (returns its length).
+long long fkr_bench_matrix_csv(long long n_queries, int k_dim, int kind, int reps, int threads,
+                               const long long* n_list, int n_count, const int* k_list, int k_count,
+                               const float* r_list, int r_count, char* out, long long cap) {
+    long long len = -1;
+    guarded([&] {
+        flatkd::BenchConfig base;
+        base.n_queries = n_queries;
+        base.k_dim = k_dim;
+        base.kind = kind == 1 ? flatkd::QueryKind::knn : flatkd::QueryKind::fcp;
+        base.reps = reps;
+        base.threads = threads;
+        auto rows = flatkd::run_bench_matrix(base, std::span<const long long>(n_list, n_count),
+                                             std::span<const int>(k_list, k_count),
+                                             std::span<const float>(r_list, r_count));
+        std::ostringstream os;
+        flatkd::write_bench_csv(os, rows);
+        const std::string s = os.str();
+        len = (long long)s.size();
+        if (out && cap > 0) {
+            const long long n = len < cap - 1 ? len : cap - 1;
+            std::memcpy(out, s.data(), std::size_t(n));
+            out[n] = 0;
+        }
+    });
+    return len;
 }
 
 uint64_t fkr_derive_stream_seed(uint64_t master, uint64_t stream) {

@@ -295,10 +295,41 @@ def run_batch_device(tree: KdTree, queries, counts, hits, options: Optional[Batc
     import torch
 
     options = options or BatchOptions()
+    if options.kind == QueryKind.knn and options.k < 1:  # batch.cpp:72-73, checked first
+        raise InvalidArgument("knn: k must be >= 1")
+    # the C ABI takes raw pointers: shapes, dtypes, layout and device are
+    # checked here so a wrong tensor raises instead of reading or writing
+    # out of bounds
+    if queries.dim() != 2:
+        raise DataError("queries: expected an (m, dim) tensor")
+    m, dim = int(queries.shape[0]), int(queries.shape[1])
+    stride = options.stride
+    checks = ((queries, torch.float32, m * dim, "queries"), (counts, torch.int32, m, "counts"),
+              (hits, None, m * stride, "hits"))
+    for t, dt, need, what in checks:
+        if not t.is_cuda:
+            raise DataError(f"{what}: expected a CUDA tensor")
+        if not t.is_contiguous():
+            raise DataError(f"{what}: expected a contiguous tensor")
+        if dt is not None and t.dtype != dt:
+            raise DataError(f"{what}: expected dtype {dt}, got {t.dtype}")
+        elems = t.numel() if dt is not None else t.numel() * t.element_size() // 8
+        if elems < need:
+            raise DataError(f"{what}: holds {elems} elements, the batch needs {need}")
+    if hits.element_size() not in (8, 4) or (hits.numel() * hits.element_size()) % 8:
+        raise DataError("hits: expected 8-byte Hit slots (int64 / float64 / 2 x int32 per slot)")
+    if per_query is not None and (not per_query.is_cuda or not per_query.is_contiguous()
+                                  or per_query.numel() * per_query.element_size() < 24 * m):
+        raise DataError("per_query: expected a contiguous CUDA tensor of m x 24 bytes")
+    dev = queries.device
+    for t in (counts, hits) + ((per_query,) if per_query is not None else ()):
+        if t.device != dev:
+            raise DataError("queries, counts, hits and per_query must be on one device")
+    if tree.replica_device() is not None and dev.index != tree.replica_device():
+        raise DataError(f"queries are on cuda:{dev.index}, the tree's first replica on "
+                        f"cuda:{tree.replica_device()}")
     if stream is None:
-        stream = torch.cuda.current_stream()
-    m = queries.shape[0]
-    dim = queries.shape[1] if queries.dim() == 2 else tree.dim()
+        stream = torch.cuda.current_stream(dev)
     st = fkd_query_stats()
     tm = fkd_timings()
     o = options.to_c()

@@ -490,6 +490,14 @@ fkd_status enqueue(const fkd_tree* t, Replica& r, Workspace* w, const float* d_q
             w->sort_tmp_bytes = need;
         }
     }
+    // require_finite(queries) (batch.cpp:79) over the WHOLE batch before any
+    // walk writes a slot: the key pass checks each sub-batch it sorts; a batch
+    // of several sub-batches, or one walked without the key pass, is scanned
+    // first.  The walk kernels exit at entry once *bad is set.
+    if (!sort || m > chunk) {
+        *launches += scan_queries(d_q, m, t->dim, w->small, id_offset, st);
+        FKD_CUDA(cudaGetLastError());
+    }
     for (int64_t base = 0; base < m; base += chunk) {
         const int64_t cm = std::min(chunk, m - base);
         WalkArgs a{};
@@ -530,7 +538,8 @@ fkd_status enqueue(const fkd_tree* t, Replica& r, Workspace* w, const float* d_q
         if (sort) {
             const int64_t half = w->key_cap / 2;
             const int rc = morton_order(a.queries, cm, t->dim, t->frame, w->keys, w->keys + half,
-                                        w->ids, w->ids + half, w->sort_tmp, w->sort_tmp_bytes, st);
+                                        w->ids, w->ids + half, w->sort_tmp, w->sort_tmp_bytes, w->small,
+                                        a.id_base, st);
             if (rc < 0) return fail(FKD_CUDA_ERROR, "morton ordering failed");
             *launches += rc;
             a.order = w->ids + half;

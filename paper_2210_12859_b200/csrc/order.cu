@@ -38,17 +38,27 @@ int morton_bits_per_dim(int dim) {
     return b;
 }
 
+// The key pass reads every query once, so it also performs the reference's
+// require_finite(queries, "queries") (batch.cpp:79): the first non-finite
+// query id goes to *bad (atomicMin), and the walk kernels that follow exit
+// at entry when *bad is set, so no result slot is written for a rejected
+// batch (the reference throws before its BatchResult exists, :82-86).
 template <int D>
-__device__ __forceinline__ uint32_t morton_key(const float* __restrict__ q, int64_t i, const MortonFrame& f) {
+__device__ __forceinline__ uint32_t morton_key(const float* __restrict__ q, int64_t i, const MortonFrame& f,
+                                               unsigned long long* bad, int64_t id_base) {
     const int b = f.bits;
     const float top = float((1u << b) - 1u);
     uint32_t c[D];
+    bool finite = true;
 #pragma unroll
     for (int d = 0; d < D; ++d) {
-        float t = (__ldg(q + i * D + d) - f.lo[d]) * f.scale[d];
-        t = fminf(fmaxf(t, 0.0f), top);  // NaN -> 0 (non-finite is reported by the walk)
+        const float v = __ldg(q + i * D + d);
+        finite &= isfinite(v);
+        float t = (v - f.lo[d]) * f.scale[d];
+        t = fminf(fmaxf(t, 0.0f), top);  // NaN -> 0 (the batch is rejected anyway)
         c[d] = uint32_t(t);
     }
+    if (!finite) atomicMin(bad, (unsigned long long)(id_base + i));
     uint32_t key = 0;
     for (int bit = b - 1; bit >= 0; --bit) {
 #pragma unroll
@@ -61,10 +71,11 @@ __device__ __forceinline__ uint32_t morton_key(const float* __restrict__ q, int6
 template <int D>
 __global__ void __launch_bounds__(256)
     morton_rank_kernel(const float* __restrict__ q, int64_t m, MortonFrame f, uint32_t* __restrict__ bins,
-                       uint32_t* __restrict__ keys, uint32_t* __restrict__ ranks) {
+                       uint32_t* __restrict__ keys, uint32_t* __restrict__ ranks, unsigned long long* bad,
+                       int64_t id_base) {
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= m) return;
-    const uint32_t key = morton_key<D>(q, i, f);
+    const uint32_t key = morton_key<D>(q, i, f, bad, id_base);
     keys[i] = key;
     ranks[i] = atomicAdd(bins + key, 1u);
 }
@@ -107,10 +118,11 @@ size_t scan_bytes(int64_t bins) {
 template <int D>
 __global__ void __launch_bounds__(256)
     morton_keys_kernel(const float* __restrict__ q, int64_t m, MortonFrame f,
-                       uint32_t* __restrict__ keys, uint32_t* __restrict__ ids) {
+                       uint32_t* __restrict__ keys, uint32_t* __restrict__ ids, unsigned long long* bad,
+                       int64_t id_base) {
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= m) return;
-    keys[i] = morton_key<D>(q, i, f);
+    keys[i] = morton_key<D>(q, i, f, bad, id_base);
     ids[i] = uint32_t(i);
 }
 
@@ -127,7 +139,7 @@ size_t morton_temp_bytes(int64_t m, int dim) {
 
 int morton_order(const float* d_queries, int64_t m, int dim, const MortonFrame& frame,
                  uint32_t* keys_in, uint32_t* keys_out, uint32_t* ids_in, uint32_t* ids_out,
-                 void* temp, size_t temp_bytes, cudaStream_t st) {
+                 void* temp, size_t temp_bytes, unsigned long long* bad, int64_t id_base, cudaStream_t st) {
     const unsigned grid = unsigned((m + 255) / 256);
     // Resolution follows the batch: about 1.7 cells per query (C3, clustered:
     // 10M queries -> 8 bits per axis, a 1.25M host-path chunk -> 7, where 8
@@ -152,7 +164,7 @@ int morton_order(const float* d_queries, int64_t m, int dim, const MortonFrame& 
         if (cudaMemsetAsync(cnt, 0, size_t(bins) * 4, st) != cudaSuccess) return -1;
         uint32_t* ranks = keys_out;
         switch (dim) {
-#define FKD_RANK(D) case D: morton_rank_kernel<D><<<grid, 256, 0, st>>>(d_queries, m, f, cnt, keys_in, ranks); break;
+#define FKD_RANK(D) case D: morton_rank_kernel<D><<<grid, 256, 0, st>>>(d_queries, m, f, cnt, keys_in, ranks, bad, id_base); break;
             FKD_RANK(1) FKD_RANK(2) FKD_RANK(3) FKD_RANK(4) FKD_RANK(5) FKD_RANK(6) FKD_RANK(7) FKD_RANK(8)
 #undef FKD_RANK
             default: return -1;
@@ -162,14 +174,14 @@ int morton_order(const float* d_queries, int64_t m, int dim, const MortonFrame& 
         return 2;  // our own launches (the scan is a library launch)
     }
     switch (dim) {
-        case 1: morton_keys_kernel<1><<<grid, 256, 0, st>>>(d_queries, m, f, keys_in, ids_in); break;
-        case 2: morton_keys_kernel<2><<<grid, 256, 0, st>>>(d_queries, m, f, keys_in, ids_in); break;
-        case 3: morton_keys_kernel<3><<<grid, 256, 0, st>>>(d_queries, m, f, keys_in, ids_in); break;
-        case 4: morton_keys_kernel<4><<<grid, 256, 0, st>>>(d_queries, m, f, keys_in, ids_in); break;
-        case 5: morton_keys_kernel<5><<<grid, 256, 0, st>>>(d_queries, m, f, keys_in, ids_in); break;
-        case 6: morton_keys_kernel<6><<<grid, 256, 0, st>>>(d_queries, m, f, keys_in, ids_in); break;
-        case 7: morton_keys_kernel<7><<<grid, 256, 0, st>>>(d_queries, m, f, keys_in, ids_in); break;
-        case 8: morton_keys_kernel<8><<<grid, 256, 0, st>>>(d_queries, m, f, keys_in, ids_in); break;
+        case 1: morton_keys_kernel<1><<<grid, 256, 0, st>>>(d_queries, m, f, keys_in, ids_in, bad, id_base); break;
+        case 2: morton_keys_kernel<2><<<grid, 256, 0, st>>>(d_queries, m, f, keys_in, ids_in, bad, id_base); break;
+        case 3: morton_keys_kernel<3><<<grid, 256, 0, st>>>(d_queries, m, f, keys_in, ids_in, bad, id_base); break;
+        case 4: morton_keys_kernel<4><<<grid, 256, 0, st>>>(d_queries, m, f, keys_in, ids_in, bad, id_base); break;
+        case 5: morton_keys_kernel<5><<<grid, 256, 0, st>>>(d_queries, m, f, keys_in, ids_in, bad, id_base); break;
+        case 6: morton_keys_kernel<6><<<grid, 256, 0, st>>>(d_queries, m, f, keys_in, ids_in, bad, id_base); break;
+        case 7: morton_keys_kernel<7><<<grid, 256, 0, st>>>(d_queries, m, f, keys_in, ids_in, bad, id_base); break;
+        case 8: morton_keys_kernel<8><<<grid, 256, 0, st>>>(d_queries, m, f, keys_in, ids_in, bad, id_base); break;
         default: return -1;
     }
     size_t bytes = temp_bytes;
@@ -177,6 +189,27 @@ int morton_order(const float* d_queries, int64_t m, int dim, const MortonFrame& 
                                                     (int)m, 0, f.bits * dim, st);
     if (e != cudaSuccess) return -1;
     return 1;  // our own launches (the CUB sort kernels are library launches)
+}
+
+// require_finite(queries, "queries") (batch.cpp:79) for batches walked
+// without the key pass: first non-finite query id -> *bad.
+__global__ void __launch_bounds__(256)
+    scan_queries_kernel(const float* __restrict__ q, int64_t m, int dim, unsigned long long* bad, int64_t id_base) {
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < m * dim; i += stride)
+        if (!isfinite(__ldg(q + i))) atomicMin(bad, (unsigned long long)(id_base + i / dim));
+}
+
+int scan_queries(const float* d_queries, int64_t m, int dim, unsigned long long* bad, int64_t id_base,
+                 cudaStream_t st) {
+    if (m <= 0 || dim <= 0) return 0;
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t want = (m * dim + 255) / 256;
+    const unsigned grid = unsigned(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(sms) * 8)));
+    scan_queries_kernel<<<grid, 256, 0, st>>>(d_queries, m, dim, bad, id_base);
+    return 1;
 }
 
 // ---- tree store ----

@@ -16,10 +16,15 @@ struct MortonFrame {
 
 int morton_bits_per_dim(int dim);
 size_t morton_temp_bytes(int64_t m, int dim);
-// Keys + counting or radix sort; ids_out receives the walk order.  Returns launches or -1.
+// Keys + counting or radix sort; ids_out receives the walk order.  The key
+// pass also records the first non-finite query (id_base + i) in *bad.
+// Returns launches or -1.
 int morton_order(const float* d_queries, int64_t m, int dim, const MortonFrame& f,
                  uint32_t* keys_in, uint32_t* keys_out, uint32_t* ids_in, uint32_t* ids_out,
-                 void* temp, size_t temp_bytes, cudaStream_t st);
+                 void* temp, size_t temp_bytes, unsigned long long* bad, int64_t id_base, cudaStream_t st);
+// First non-finite query (id_base + i) -> *bad, for batches walked without the key pass.
+int scan_queries(const float* d_queries, int64_t m, int dim, unsigned long long* bad, int64_t id_base,
+                 cudaStream_t st);
 
 int pack_nodes(const float* d_src, int64_t n, int dim, int stride, float* d_dst, cudaStream_t st);
 int tree_scan(const float* d_src, int64_t n, int dim, unsigned* d_lohi, unsigned long long* d_bad,

@@ -367,6 +367,12 @@ struct LaneWalk {
                 pd = pick(p, d);
             } else {
                 pd = __ldg(a.nodes + size_t(curr) * S + d);
+                // a return trip loads only the split coordinate; the distance
+                // below is formed every trip but used only on a first visit.
+                // The empty asm defines p (an unspecified value, no
+                // instruction) so no indeterminate value is ever read.
+#pragma unroll
+                for (int j = 0; j < D; ++j) asm("" : "=f"(p[j]));
             }
         } else if constexpr (S > D) {
             load_point<D, S>(a.nodes, curr, p, &pd);  // split plane from the padding slot
@@ -688,6 +694,7 @@ __device__ __forceinline__ bool walk_budgeted(W& w, const WalkArgs& a, int trips
 // One thread per walk position (plain grid).
 template <int D, int S, int KB, bool STATS, bool UNORDERED>
 __global__ void __launch_bounds__(kWalkThreads, walk_min_blocks<D, KB>()) walk_kernel(const WalkArgs a) {
+    if (*a.bad != kNoBad) return;  // a rejected batch (batch.cpp:79) writes no slot
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     LaneWalk<D, S, KB, STATS, UNORDERED> w;
     bool active = i < a.m && w.init(a, i);
@@ -767,6 +774,7 @@ struct QueryRegs {
 
 template <int D, bool STATS, bool UNORDERED>
 __global__ void __launch_bounds__(128) walk_heap_kernel(const WalkArgs a) {
+    if (*a.bad != kNoBad) return;  // a rejected batch (batch.cpp:79) writes no slot
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     bool active = i < a.m;
     int64_t qi = 0;

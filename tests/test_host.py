@@ -96,3 +96,30 @@ def test_cpp_shim_headers_compile(tmp_path):
 def test_validation_order_in_options():
     with pytest.raises(fk.InvalidArgument):
         fk.run_batch(None, np.zeros((1, 3), np.float32), fk.BatchOptions(kind=fk.QueryKind.knn, k=0))
+
+
+def test_workload_generators_match_reference_rng(reference):
+    """bench.py's reference arm draws its inputs from the reference library
+    (oracle/ref_capi.cpp) and the B200 arm from the product's host
+    generators: both must be byte-identical, uniform and clustered."""
+    for dim in (2, 3, 8):
+        assert np.array_equal(fk.random_points(1, 2, 5000, dim), reference.stream_points(1, 2, 5000, dim))
+        assert np.array_equal(fk.clustered_points(1, 1, 5000, dim, 64, 0.02),
+                              reference.clustered_points(1, 1, 5000, dim, 64, 0.02))
+
+
+def test_scale_goldens_agree_with_survey():
+    """tests/golden/scale.json (reference run over the whole batches) against
+    the hashes SURVEY.md §8(c) recorded at survey time."""
+    import json
+
+    g = json.load(open(os.path.join(ROOT, "tests", "golden", "scale.json")))["cases"]
+    survey = {"fcp_3d_n10m_m1m": "0cca445a11013618", "knn8_3d_n10m_m1m": "5a71a6a204bbe790",
+              "fcp_4d_n10m_m1m": "11d43fd7c68c62e6", "knn8_4d_n10m_m1m_r0.01": "7c5c62b9b41500e3",
+              "knn16_2d_n10m_m200k": "6a39ab1bb32b6cb2", "knn16_4d_n10m_m200k": "563944befa0aff8b",
+              "knn16_8d_n10m_m200k": "10a6147e5f8a5a07", "fcp_3d_n100m_m200k": "1fc44d5457a0fee4"}
+    for name, h in survey.items():
+        assert g[name]["hash"] == h, name
+    assert {"c3_fcp_clustered_n10m_m10m", "c3_knn8_clustered_n10m_m10m"} <= set(g)
+    # P-bar of the C3 batches (bench.py's algorithmic bytes) from the reference's counters
+    assert abs(g["c3_knn8_clustered_n10m_m10m"]["stats"][2] / 1e7 - 126.4611659) < 1e-6
