@@ -113,6 +113,17 @@ fkd_status fkd_tree_create_device(const float* d_level_order, int64_t n, int32_t
 void fkd_tree_destroy(fkd_tree* tree);
 int64_t fkd_tree_size(const fkd_tree* tree);
 int32_t fkd_tree_dim(const fkd_tree* tree);
+/* Devices holding a replica of the tree store, in shard order: writes up to
+ * `cap` device ids to `devices` (may be NULL) and returns the replica count.
+ * fkd_run_batch_device runs on the first one. */
+int32_t fkd_tree_replicas(const fkd_tree* tree, int32_t* devices, int32_t cap);
+
+/* Adds replicas of the tree store on `devices` (appended to the shard
+ * order), copied device to device from the existing replicas as a pipelined
+ * chain over NVLink / NVSwitch (64 MB pieces; cudaMemcpyPeerAsync staging
+ * through the host where a pair has no peer access).  Not thread-safe with
+ * concurrent queries on the same tree. */
+fkd_status fkd_tree_add_replicas(fkd_tree* tree, const int32_t* devices, int32_t ndev);
 
 /* ---- the batch query path (replaces flatkd::run_batch, batch.cpp:71-134) ----
  * Host buffers: queries[m*dim] row-major; counts[m]; hits[m*stride];

@@ -214,6 +214,24 @@ class KdTree:
     def nodes(self) -> Optional[np.ndarray]:
         return self._nodes
 
+    def replica_devices(self) -> List[int]:
+        """CUDA devices holding a replica of the tree store (shard order)."""
+        n = int(LIB.fkd_tree_replicas(self._h, None, 0))
+        out = (C.c_int32 * max(n, 1))()
+        LIB.fkd_tree_replicas(self._h, out, n)
+        return [int(out[i]) for i in range(n)]
+
+    def add_replicas(self, devices: Sequence[int]) -> None:
+        """Replicate the tree store onto more devices, device to device
+        (pipelined chain over NVLink / NVSwitch); they join the shard order."""
+        devs = (C.c_int32 * max(len(devices), 1))(*devices)
+        _check(LIB.fkd_tree_add_replicas(self._h, devs, len(devices)))
+
+    def replica_device(self) -> Optional[int]:
+        """The device fkd_run_batch_device runs on (the first replica)."""
+        devs = self.replica_devices()
+        return devs[0] if devs else None
+
     @property
     def handle(self):
         return self._h

@@ -6,7 +6,9 @@
 // No CPU fallback exists: every query is answered by the sm_100a kernels in
 // walk.cuh; without a usable device the calls fail with FKD_NO_DEVICE.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
+#include <memory>
 #include <condition_variable>
 #include <cstdio>
 #include <cstdlib>
@@ -20,6 +22,7 @@
 
 #include "fkd_b200.h"
 #include "build.cuh"
+#include "knobs.hpp"
 #include "order.cuh"
 #include "trace.cuh"
 #include "walk.cuh"
@@ -44,28 +47,6 @@ fkd_status fail(fkd_status s, const std::string& msg) {
 
 constexpr int64_t kSortChunk = int64_t(1) << 30;  // u32 ids, int item counts in CUB
 
-struct Tuning {
-    int budget = -1;  // -1: per kind (first_budget: fcp 112, kNN <= 4 slots 256, larger lists 3072 loop trips)
-    int64_t resume_min = 0;  // 0: SMs x 64 (measured: 8-D and 4-D kNN64 tails; C3's ~2k stay on the CTA pass)
-    int resume_trips = 0;    // 0: fcp 4096, kNN 49152 (measured on 8-D); <0: unbounded
-    // continuation rounds after the budgeted walk (walk_round_kernel), trips
-    // per round.  Measured (tools/rounds_ab.sh, tools/rounds_knn_ab.sh,
-    // profiles/r01e_rounds_*): fcp walk -14% (3-D C3) to -30% (4-D), kNN4
-    // 4-D -18%, kNN8 walk + tail -3% (C3) / -7% (4-D) / +1% (3-D uniform);
-    // for lists of >= 16 slots parking costs more than the denser warps save
-    // (2-D kNN16 +2%, 4-D kNN20 +48%), so those keep one long budgeted walk.
-    std::vector<int> rounds_fcp{112, 224, 448}, rounds_knn4{256, 512}, rounds_knn8{384, 768, 1536};
-    // fcp batches below 2^22 queries stop after two rounds: their few parked walks
-    // finish sooner in the CTA pass than in a latency-bound 448-trip round
-    // (clustered 1.25M / 2.5M: -22% / -13%; 1M uniform -1%), while at 10M the third
-    // round keeps the resume pass off (C3 fcp 2.49 vs 3.03 ms without it)
-    // (tools/fcp_small_ab.sh, tools/fcp_rounds_c3_ab.sh, profiles/r01i_fcp_*ab.log)
-    std::vector<int> rounds_fcp_small{112, 224};
-    bool rounds_fcp_env = false;  // FKD_RROUNDS_FCP given: every batch size
-    std::vector<int> rounds_knn_env;
-    bool rounds_knn_all = false;  // FKD_RROUNDS_KNN given: every kNN bucket
-};
-
 int walk_bucket_of(int k);
 // The rounds run for register lists of <= 4 slots (fcp, k <= 4) and, in
 // batches of >= 2^22 queries, 8 slots (a 1M-query kNN8 batch is 4-8% slower
@@ -85,48 +66,31 @@ inline int first_budget(int k, int64_t m) {
 // 4-D kNN16/50/64 and 5-D kNN16 finish inside 12288 (unchanged); tools/tail8d_ab2.sh
 inline int resume_trips_default(int k) { return k == 1 ? 4096 : 49152; }
 
-std::vector<int> parse_ints(const char* e) {
-    std::vector<int> v;
-    for (const char* p = e; *p;) {
-        const int x = std::atoi(p);
-        if (x > 0) v.push_back(x);
-        while (*p && *p != ',') ++p;
-        if (*p == ',') ++p;
-    }
-    return v;
+// Continuation-round schedule (knobs.hpp): measured (tools/rounds_ab.sh,
+// tools/rounds_knn_ab.sh, profiles/r01e_rounds_*): fcp walk -14% (3-D C3) to
+// -30% (4-D), kNN4 4-D -18%, kNN8 walk + tail -3% (C3) / -7% (4-D); for lists
+// of >= 16 slots parking costs more than the denser warps save (2-D kNN16 +2%,
+// 4-D kNN20 +48%), so those keep one long budgeted walk.  fcp batches below
+// 2^22 queries stop after two rounds: their few parked walks finish sooner in
+// the CTA pass than in a latency-bound 448-trip round (clustered 1.25M / 2.5M:
+// -22% / -13%), while at 10M the third round keeps the resume pass off (C3 fcp
+// 2.49 vs 3.03 ms without it; profiles/r01i_fcp_*ab.log).
+const std::vector<int>& round_schedule(const Knobs& kn, int k, int64_t m) {
+    static const std::vector<int> none;
+    if (k == 1) return (kn.rounds_fcp_env || m >= (int64_t(1) << 22)) ? kn.rounds_fcp : kn.rounds_fcp_small;
+    if (kn.rounds_knn_all) return kn.rounds_knn_env;
+    if (!rounds_on(k, m)) return none;
+    return walk_bucket_of(k) <= 4 ? kn.rounds_knn4 : kn.rounds_knn8;
 }
 
-// Launch tuning, overridable per call for experiments and tests:
-// FKD_BUDGET=<first walk's loop trips before a query parks; <0 per kind, 0 off>,
-// FKD_RROUNDS_FCP / FKD_RROUNDS_KNN=<t1,t2,..> (continuation rounds; "0": none),
-// FKD_RESUME_MIN=<overflow count that selects the resume pass>,
-// FKD_RESUME_TRIPS=<steps the resume pass adds before the CTA pass; <0 unbounded>,
-Tuning tuning() {
-    return [] {
-        Tuning x;
-        if (const char* e = std::getenv("FKD_BUDGET")) x.budget = std::atoi(e);  // <0: per kind, 0: off
-        if (const char* e = std::getenv("FKD_RESUME_MIN")) x.resume_min = std::atoll(e);
-        if (const char* e = std::getenv("FKD_RESUME_TRIPS")) x.resume_trips = std::atoi(e);
-        if (const char* e = std::getenv("FKD_RROUNDS_FCP")) {
-            x.rounds_fcp = parse_ints(e);
-            x.rounds_fcp_env = true;
-        }
-        if (const char* e = std::getenv("FKD_RROUNDS_KNN")) {
-            x.rounds_knn_env = parse_ints(e);
-            x.rounds_knn_all = true;
-        }
-        return x;
-    }();
-}
-
-// Store layout: padded vectors (1, 4, 4, 4, 8, 8, 8, 8 floats) by default;
-// FKD_LAYOUT=packed keeps 2-D and 3-D nodes at 8 and 12 bytes (SURVEY §7
-// step 3: chosen by measurement, see DESIGN.md).
+// Store layout: padded vectors (1, 4, 4, 4, 8, 8, 8, 8 floats); building with
+// -DFKD_PACKED_LAYOUT=1 keeps 2-D and 3-D nodes at 8 and 12 bytes (SURVEY §7
+// step 3: chosen by measurement, DESIGN.md §2).
+#ifndef FKD_PACKED_LAYOUT
+#define FKD_PACKED_LAYOUT 0
+#endif
 int store_stride(int dim) {
-    static const bool packed = [] {
-        const char* e = std::getenv("FKD_LAYOUT");
-        return e && std::strcmp(e, "packed") == 0;
-    }();
+    constexpr bool packed = FKD_PACKED_LAYOUT != 0;
     switch (dim) {
         case 1: return 1;
         case 2: return packed ? 2 : 4;  // 16-byte nodes with the split plane: 2-D kNN16 -1%, fcp -3%
@@ -308,6 +272,69 @@ void par_copy(void* dst, const void* src, size_t bytes) {
     });
 }
 
+// First non-finite float of p[0, count) or -1 (require_finite, point.hpp:59-63:
+// a float is non-finite iff its exponent bits are all ones).  The block OR is
+// branch-free so the compiler vectorises it; the exact index is searched
+// only inside a block that has one.
+int64_t first_nonfinite(const float* p, int64_t count) {
+    const uint32_t* u = reinterpret_cast<const uint32_t*>(p);
+    constexpr int64_t kBlock = 4096;
+    for (int64_t b = 0; b < count; b += kBlock) {
+        const int64_t e = std::min(count, b + kBlock);
+        uint32_t any = 0;
+        for (int64_t i = b; i < e; ++i) any |= uint32_t((u[i] & 0x7f800000u) == 0x7f800000u);
+        if (any)
+            for (int64_t i = b; i < e; ++i)
+                if ((u[i] & 0x7f800000u) == 0x7f800000u) return i;
+    }
+    return -1;
+}
+
+// par_copy + first_nonfinite of the copied floats (dst is cache-hot per
+// 256 KB piece).  Returns the first non-finite float index or -1.
+int64_t par_copy_check(float* dst, const float* src, int64_t count) {
+    if (count <= 0) return -1;
+    CopyPool& pool = CopyPool::get();
+    const size_t bytes = size_t(count) * sizeof(float);
+    const int parts = bytes < (size_t(4) << 20) ? 1 : pool.parts();
+    const int64_t per = ((count + parts - 1) / parts + 1023) & ~int64_t(1023);
+    std::vector<int64_t> first(size_t(parts), -1);
+    auto part = [&](int i) {
+        const int64_t lo = std::min(count, int64_t(i) * per), hi = std::min(count, lo + per);
+        constexpr int64_t kPiece = 65536;  // floats
+        for (int64_t b = lo; b < hi; b += kPiece) {
+            const int64_t n = std::min(kPiece, hi - b);
+            std::memcpy(dst + b, src + b, size_t(n) * sizeof(float));
+            if (first[size_t(i)] < 0) {
+                const int64_t f = first_nonfinite(dst + b, n);
+                if (f >= 0) first[size_t(i)] = b + f;
+            }
+        }
+    };
+    if (parts == 1) part(0); else pool.run(parts, part);
+    for (int64_t f : first)
+        if (f >= 0) return f;
+    return -1;
+}
+
+// first_nonfinite over the copy pool (read-only).
+int64_t par_check(const float* src, int64_t count) {
+    if (count <= 0) return -1;
+    CopyPool& pool = CopyPool::get();
+    const int parts = count < (int64_t(1) << 20) ? 1 : pool.parts();
+    const int64_t per = ((count + parts - 1) / parts + 1023) & ~int64_t(1023);
+    std::vector<int64_t> first(size_t(parts), -1);
+    auto part = [&](int i) {
+        const int64_t lo = std::min(count, int64_t(i) * per), hi = std::min(count, lo + per);
+        const int64_t f = first_nonfinite(src + lo, hi - lo);
+        if (f >= 0) first[size_t(i)] = lo + f;
+    };
+    if (parts == 1) part(0); else pool.run(parts, part);
+    for (int64_t f : first)
+        if (f >= 0) return f;
+    return -1;
+}
+
 bool is_pageable(const void* p) {
     cudaPointerAttributes at{};
     if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
@@ -345,10 +372,31 @@ cudaError_t acquire_stage(size_t bytes, HostStage* out) {
     return e;
 }
 
+// The pool keeps at most kStagePoolMax buffers of at most kStageKeepMax
+// bytes each; anything else goes back to the OS at release, so a huge batch
+// never leaves gigabytes pinned (staging is a bounded per-chunk ring, so a
+// call needs at most slots x chunk bytes).
+constexpr size_t kStageKeepMax = size_t(2) << 30;
+constexpr size_t kStagePoolMax = 8;
+
 void release_stage(HostStage s) {
     if (!s.p) return;
-    std::lock_guard<std::mutex> lk(g_stage_mu);
-    g_stage_pool.push_back(s);
+    if (s.cap > kStageKeepMax) {
+        cudaFreeHost(s.p);
+        return;
+    }
+    HostStage drop{};
+    {
+        std::lock_guard<std::mutex> lk(g_stage_mu);
+        g_stage_pool.push_back(s);
+        if (g_stage_pool.size() > kStagePoolMax) {
+            auto smallest = std::min_element(g_stage_pool.begin(), g_stage_pool.end(),
+                                             [](const HostStage& a, const HostStage& b) { return a.cap < b.cap; });
+            drop = *smallest;
+            g_stage_pool.erase(smallest);
+        }
+    }
+    if (drop.p) cudaFreeHost(drop.p);
 }
 
 }  // namespace
@@ -410,12 +458,12 @@ void release_ws(Replica& r, Workspace* w) {
     r.pool.push_back(w);
 }
 
+// Largest k on a register list (larger k: the heap kernel).
+#ifndef FKD_REG_MAXK
+#define FKD_REG_MAXK 64
+#endif
 int walk_bucket_of(int k) {
-    static const int reg_max = [] {  // experiment: route larger k to the heap kernel
-        const char* e = std::getenv("FKD_REG_MAXK");
-        return e ? std::atoi(e) : 64;
-    }();
-    if (k > reg_max) return 0;
+    if (k > FKD_REG_MAXK) return 0;
     if (k <= 1) return 1;
     if (k <= 2) return 2;
     if (k <= 4) return 4;
@@ -460,7 +508,7 @@ bool use_morton(const fkd_tree* t, const fkd_batch_options* o, int64_t m) {
 fkd_status enqueue(const fkd_tree* t, Replica& r, Workspace* w, const float* d_q, int64_t m,
                    const fkd_batch_options* o, float cap2, int32_t* d_counts, fkd_hit* d_hits,
                    fkd_query_stats* d_per_query, bool stats, cudaStream_t st, int* launches,
-                   int* walk_launches, cudaEvent_t ev_mid, cudaEvent_t ev_tail = nullptr,
+                   int* walk_launches, const Knobs& tu, cudaEvent_t ev_mid, cudaEvent_t ev_tail = nullptr,
                    int64_t id_offset = 0, cudaStream_t tail_st = nullptr, int budget_div = 1) {
     const int k = o->kind == FKD_KNN ? o->k : 1;
     if (t->n == 0) {  // every query returns empty; queries are not read (batch.cpp:75)
@@ -516,7 +564,6 @@ fkd_status enqueue(const fkd_tree* t, Replica& r, Workspace* w, const float* d_q
         a.per_query = d_per_query ? d_per_query + base : nullptr;
         a.bad = w->small;
         a.id_base = id_offset + base;
-        const Tuning tu = tuning();
         int budget = tu.budget >= 0 ? tu.budget : first_budget(k, cm);
         if (budget_div > 1 && budget > 0) budget = std::max(64, budget / budget_div);
         a.budget = (stats || walk_bucket_of(k) == 0 || t->dim > 8) ? 0 : budget;
@@ -559,12 +606,7 @@ fkd_status enqueue(const fkd_tree* t, Replica& r, Workspace* w, const float* d_q
                 FKD_CUDA(cudaStreamWaitEvent(tail_st, w->pe[3], 0));
             }
             const cudaStream_t ts = (a.budget > 0 && tail_st) ? tail_st : st;
-            static const std::vector<int> none;
-            const std::vector<int>& rounds =
-                k == 1 ? ((tu.rounds_fcp_env || cm >= (int64_t(1) << 22)) ? tu.rounds_fcp : tu.rounds_fcp_small)
-                       : (tu.rounds_knn_all ? tu.rounds_knn_env
-                                            : (!rounds_on(k, cm) ? none
-                                                             : (walk_bucket_of(k) <= 4 ? tu.rounds_knn4 : tu.rounds_knn8)));
+            const std::vector<int>& rounds = round_schedule(tu, k, cm);
             if (a.budget > 0 && !rounds.empty()) {
                 // continuation rounds: the parked walks, compacted into dense
                 // warps, continue for `trips` more trips per round; lists
@@ -673,6 +715,13 @@ void fkd_host_free(void* p) { cudaFreeHost(p); }
 int64_t fkd_tree_size(const fkd_tree* t) { return t ? t->n : 0; }
 int32_t fkd_tree_dim(const fkd_tree* t) { return t ? t->dim : 0; }
 
+int32_t fkd_tree_replicas(const fkd_tree* t, int32_t* devices, int32_t cap) {
+    if (!t) return 0;
+    const int32_t n = int32_t(t->reps.size());
+    for (int32_t i = 0; devices && i < n && i < cap; ++i) devices[i] = t->reps[i]->device;
+    return n;
+}
+
 void fkd_tree_destroy(fkd_tree* t) {
     if (!t) return;
     for (Replica* r : t->reps) delete r;
@@ -682,8 +731,6 @@ void fkd_tree_destroy(fkd_tree* t) {
 static fkd_status set_frame(fkd_tree* t, const float* lo, const float* hi) {
     const int dim = t->dim;
     t->frame.bits = morton_bits_per_dim(std::min(dim, 8));
-    if (const char* e = std::getenv("FKD_MORTON_BITS"))  // experiment: bits per axis
-        t->frame.bits = std::max(1, std::min(t->frame.bits, std::atoi(e)));
     const float top = float((1u << t->frame.bits) - 1u);
     for (int d = 0; d < 8; ++d) {
         t->frame.lo[d] = 0.0f;
@@ -702,15 +749,12 @@ static fkd_status set_frame(fkd_tree* t, const float* lo, const float* hi) {
 // nodes: one 32-byte sector) instead of straddling two, so the far child's
 // sector usually arrived with the close child's.  Measured
 // (tools/node_shift_ab.sh, profiles/r01j_node_shift_ab.log): C3 kNN8 walk
-// -1.6%, fcp -1.5%, uniform kNN8 -0.8%, 4-D kNN16 -1%; FKD_NODE_SHIFT=0
+// -1.6%, fcp -1.5%, uniform kNN8 -0.8%, 4-D kNN16 -1%; -DFKD_NODE_SHIFT=0
 // restores the unshifted store.
-static int64_t node_shift() {
-    static const int64_t v = [] {
-        const char* e = std::getenv("FKD_NODE_SHIFT");
-        return e ? int64_t(std::max(0, std::min(8, std::atoi(e)))) : int64_t(1);
-    }();
-    return v;
-}
+#ifndef FKD_NODE_SHIFT
+#define FKD_NODE_SHIFT 1
+#endif
+static int64_t node_shift() { return FKD_NODE_SHIFT; }
 
 static fkd_status alloc_store(Replica* r, int64_t n, int stride) {
     const int64_t sh = node_shift();
@@ -752,31 +796,84 @@ static fkd_status make_replica(fkd_tree* t, int dev, const float* src, bool src_
     return FKD_OK;
 }
 
-// Further replicas are copied device to device from the first one (over
-// NVLink / NVSwitch between B200s; cudaMemcpyPeer stages through the host
-// only when peer access is unavailable) — SURVEY §8(e): one upload, then a
-// fan-out of the packed store.
-static fkd_status peer_replica(fkd_tree* t, int dev) {
-    Replica* src = t->reps.front();
-    auto* r = new Replica();
-    r->device = dev;
-    t->reps.push_back(r);
-    if (t->n == 0) return FKD_OK;
-    const size_t bytes = size_t(t->n) * t->stride * sizeof(float);
-    DeviceGuard g(dev);
-    if (fkd_status e = alloc_store(r, t->n, t->stride); e != FKD_OK) return e;
-    if (dev == src->device) {
-        FKD_CUDA(cudaMemcpy(r->nodes, src->nodes, bytes, cudaMemcpyDeviceToDevice));
-    } else {
-        int can = 0;
-        cudaDeviceCanAccessPeer(&can, dev, src->device);
-        if (can) {
-            cudaError_t e = cudaDeviceEnablePeerAccess(src->device, 0);
-            if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
-        }
-        FKD_CUDA(cudaMemcpyPeer(r->nodes, dev, src->nodes, src->device, bytes));
+// Further replicas are copied device to device from the first one — one
+// upload, then a fan-out of the packed store over NVLink / NVSwitch (SURVEY
+// §8(e)).  The fan-out is a pipelined chain, the way a ring broadcast moves
+// data: the store is cut into kFanChunk pieces and piece c hops
+// dev[0] -> dev[1] -> ... -> dev[R], each hop on a stream of its destination
+// device, starting as soon as piece c has arrived at the hop's source.  Every
+// GPU sends and receives each byte once, so on NVSwitch (full bandwidth to
+// every peer) the whole fan-out takes about (store + R x piece) / link rate
+// instead of R store copies back to back (1.6 GB at C5, 8 GPUs: ~2.5 ms
+// rather than ~12 ms one after another from device 0).  Peer access is
+// enabled where the pair supports it; cudaMemcpyPeerAsync stages through the
+// host otherwise.
+static constexpr size_t kFanChunk = size_t(64) << 20;
+
+static fkd_status fanout_replicas(fkd_tree* t, const std::vector<int>& devs) {
+    if (devs.empty()) return FKD_OK;
+    std::vector<Replica*> chain{t->reps.front()};
+    for (int dev : devs) {
+        auto* r = new Replica();
+        r->device = dev;
+        t->reps.push_back(r);
+        chain.push_back(r);
     }
-    return FKD_OK;
+    if (t->n == 0) return FKD_OK;
+    const size_t bytes = size_t(t->n + node_shift()) * t->stride * sizeof(float);
+    for (size_t i = 1; i < chain.size(); ++i) {
+        DeviceGuard g(chain[i]->device);
+        if (fkd_status e = alloc_store(chain[i], t->n, t->stride); e != FKD_OK) return e;
+        const int src = chain[i - 1]->device, dst = chain[i]->device;
+        if (src != dst) {
+            int can = 0;
+            cudaDeviceCanAccessPeer(&can, dst, src);
+            if (can) {
+                cudaError_t e = cudaDeviceEnablePeerAccess(src, 0);
+                if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+                else if (e != cudaSuccess) return fail(FKD_CUDA_ERROR, std::string("peer access: ") + cudaGetErrorString(e));
+            }
+        }
+    }
+    const size_t pieces = (bytes + kFanChunk - 1) / kFanChunk;
+    const size_t hops = chain.size() - 1;
+    std::vector<cudaStream_t> st(hops, nullptr);
+    std::vector<cudaEvent_t> arrived(hops * pieces, nullptr);  // piece c at chain[h + 1]
+    fkd_status err = FKD_OK;
+    auto cuda = [&](cudaError_t e, const char* what) {
+        if (e != cudaSuccess && err == FKD_OK) err = fail(FKD_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+        return e == cudaSuccess;
+    };
+    for (size_t h = 0; h < hops && err == FKD_OK; ++h) {
+        DeviceGuard g(chain[h + 1]->device);
+        cuda(cudaStreamCreateWithFlags(&st[h], cudaStreamNonBlocking), "fan-out stream");
+        for (size_t c = 0; c < pieces && err == FKD_OK; ++c)
+            cuda(cudaEventCreateWithFlags(&arrived[h * pieces + c], cudaEventDisableTiming), "fan-out event");
+    }
+    // enqueue piece-major so every hop's stream sees its pieces in order and
+    // the waits name events recorded earlier in host order
+    for (size_t c = 0; c < pieces && err == FKD_OK; ++c) {
+        const size_t off = c * kFanChunk, len = std::min(kFanChunk, bytes - off);
+        for (size_t h = 0; h < hops && err == FKD_OK; ++h) {
+            DeviceGuard g(chain[h + 1]->device);
+            if (h > 0 && !cuda(cudaStreamWaitEvent(st[h], arrived[(h - 1) * pieces + c], 0), "fan-out wait")) break;
+            const char* from = reinterpret_cast<const char*>(chain[h]->alloc) + off;
+            char* to = reinterpret_cast<char*>(chain[h + 1]->alloc) + off;
+            if (!cuda(cudaMemcpyPeerAsync(to, chain[h + 1]->device, from, chain[h]->device, len, st[h]),
+                      "fan-out copy"))
+                break;
+            cuda(cudaEventRecord(arrived[h * pieces + c], st[h]), "fan-out event");
+        }
+    }
+    for (size_t h = 0; h < hops; ++h) {
+        if (!st[h]) continue;
+        DeviceGuard g(chain[h + 1]->device);
+        cuda(cudaStreamSynchronize(st[h]), "fan-out");
+        cudaStreamDestroy(st[h]);
+    }
+    for (auto& e : arrived)
+        if (e) cudaEventDestroy(e);
+    return err;
 }
 
 fkd_status fkd_tree_create(const float* level_order, int64_t n, int32_t dim,
@@ -814,20 +911,32 @@ fkd_status fkd_tree_create(const float* level_order, int64_t n, int32_t dim,
         cudaGetDevice(&cur);
         devs.push_back(cur);
     }
-    for (size_t i = 0; i < devs.size(); ++i) {
-        const int dev = devs[i];
+    for (const int dev : devs)
         if (dev < 0 || dev >= count) {
             fkd_tree_destroy(t);
             return fail(FKD_INVALID_ARGUMENT, "device id out of range");
         }
-        fkd_status s = i == 0 ? make_replica(t, dev, level_order, false, nullptr) : peer_replica(t, dev);
-        if (s != FKD_OK) {
-            fkd_tree_destroy(t);
-            return s;
-        }
+    fkd_status s = make_replica(t, devs[0], level_order, false, nullptr);
+    if (s == FKD_OK) s = fanout_replicas(t, std::vector<int>(devs.begin() + 1, devs.end()));
+    if (s != FKD_OK) {
+        fkd_tree_destroy(t);
+        return s;
     }
     *out = t;
     return FKD_OK;
+}
+
+fkd_status fkd_tree_add_replicas(fkd_tree* t, const int32_t* devices, int32_t ndev) {
+    if (!t) return fail(FKD_INVALID_ARGUMENT, "null tree");
+    if (t->reps.empty()) return fail(FKD_NO_DEVICE, "tree has no device replica");
+    if (ndev <= 0) return FKD_OK;
+    if (!devices) return fail(FKD_INVALID_ARGUMENT, "null device list");
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+        return fail(FKD_NO_DEVICE, "no CUDA device visible (the B200 path has no CPU fallback)");
+    for (int32_t i = 0; i < ndev; ++i)
+        if (devices[i] < 0 || devices[i] >= count) return fail(FKD_INVALID_ARGUMENT, "device id out of range");
+    return fanout_replicas(t, std::vector<int>(devices, devices + ndev));
 }
 
 fkd_status fkd_tree_create_device(const float* d_level_order, int64_t n, int32_t dim, void* stream,
@@ -992,12 +1101,13 @@ fkd_status fkd_run_batch_device(const fkd_tree* t, const float* d_q, int64_t m, 
     Workspace* w = nullptr;
     if ((s = acquire_ws(r, &w)) != FKD_OK) return s;
     const bool want_stats = stats != nullptr || d_per_query != nullptr;
+    const Knobs kn = read_knobs();
     int launches = 0, walk_launches = 0;
     auto body = [&]() -> fkd_status {
         FKD_CUDA(reset_small(w, st));
         if (timings) FKD_CUDA(cudaEventRecord(w->ev[0], st));
         fkd_status e = enqueue(t, r, w, d_q, m, o, cap2, d_counts, d_hits, d_per_query, want_stats,
-                               st, &launches, &walk_launches, timings ? w->ev[1] : nullptr,
+                               st, &launches, &walk_launches, kn, timings ? w->ev[1] : nullptr,
                                timings ? w->ev[3] : nullptr);
         if (e != FKD_OK) return e;
         if (timings) FKD_CUDA(cudaEventRecord(w->ev[2], st));
@@ -1024,10 +1134,127 @@ fkd_status fkd_run_batch_device(const fkd_tree* t, const float* d_q, int64_t m, 
     return s;
 }
 
-// Host-buffer path: shard over the tree's devices, and per device split the
-// shard into chunks that alternate between two workspaces (two streams) so
-// the H2D copy of one chunk, the walk of another and the D2H copy of a third
-// overlap.  Counts and hits land directly in the caller's buffers.
+}  // extern "C"
+
+// ---- host-buffer path (fkd_run_batch) --------------------------------------
+//
+// The batch is sharded over the tree's devices in contiguous blocks (the
+// reference's OpenMP loop over queries, batch.cpp:93-103, lifted to devices);
+// each device's shard runs as its own pipeline, enqueued by its own host
+// thread.  Per device, the shard is cut into a graduated chunk schedule —
+// small first chunks (the first H2D + walk overlap nothing), shard/8 middle
+// chunks, small last chunks (the last D2H overlaps nothing) — walked on
+// `streams` slot streams so the H2D engine, the SMs and the D2H engine stay
+// busy at once:
+//   copy-in stream : H2D chunk c                       -> ev_in[c]
+//   slot stream    : wait ev_in[c]; order + walk       -> ev_walk[c]
+//   copy-out stream: wait ev_walk[c]; D2H counts, hits -> ev_out[c]
+// Device staging is "full" when the shard's queries and results fit in a
+// quarter of the free memory (all H2Ds are then issued up front, so the
+// copy-in finishes before it shares PCIe with the copy-out); otherwise each
+// slot holds its largest chunk and chunk c reuses slot c mod R after the
+// slot's previous walk / D2H.
+//
+// Pageable caller buffers (std::vector / NumPy: what a reference caller
+// holds) are staged through bounded rings of pinned host slots: a query
+// chunk is copied into its ring slot by the host copy pool just before its
+// H2D (the copy also runs require_finite, batch.cpp:79), and a drain thread
+// enqueues each chunk's D2H into a result ring slot and copies the slot out
+// to the caller once the D2H has landed, R chunks behind.  Results reach the
+// caller's buffers only after every query of the batch passed the host check,
+// so a rejected batch leaves pageable outputs untouched, as the reference
+// throws before its BatchResult exists (batch.cpp:79 before :82-86).
+// Without a pinned ring (allocation failure, FKD_PAGEABLE_STAGING=0) the
+// pageable pointers go to cudaMemcpyAsync directly.
+namespace fkd {
+namespace {
+
+constexpr int kHostRing = 4;  // pinned staging slots per direction per device
+
+struct PipeJob {
+    int64_t base, count, off;  // global query offset, size, offset in the device's shard
+    int ws;                    // slot (workspace) index
+};
+
+struct DevicePipe {
+    int di = 0;
+    Replica* rep = nullptr;
+    std::vector<Workspace*> wss;
+    std::vector<PipeJob> jobs;
+    bool full = false;
+    bool pg_q = false, pg_out = false;
+    HostStage qst{}, rst{};
+    int64_t max_chunk = 0;
+    size_t r_slot_bytes = 0;
+    std::vector<cudaEvent_t> ev_in, ev_walk, ev_out;
+    // enqueue thread -> drain thread hand-off
+    std::mutex mu;
+    std::condition_variable cv;
+    size_t enqueued = 0, d2h_enqueued = 0;
+    bool enq_done = false;
+};
+
+struct PipeShared {
+    std::mutex mu;
+    std::condition_variable cv;
+    fkd_status err = FKD_OK;
+    std::string msg;
+    std::atomic<bool> stop{false};
+    int checks_left = 0;                   // enqueue threads still running their host checks
+    unsigned long long host_bad = kNoBad;  // first non-finite query found on the host
+
+    void error(fkd_status s, const std::string& m) {
+        std::lock_guard<std::mutex> lk(mu);
+        if (err == FKD_OK) {
+            err = s;
+            msg = m;
+        }
+        stop = true;
+        cv.notify_all();
+    }
+    void bad(unsigned long long id) {
+        std::lock_guard<std::mutex> lk(mu);
+        host_bad = std::min(host_bad, id);
+    }
+    void checks_done() {
+        std::lock_guard<std::mutex> lk(mu);
+        --checks_left;
+        cv.notify_all();
+    }
+    bool wait_checks() {  // true: every query passed and nothing failed
+        std::unique_lock<std::mutex> lk(mu);
+        cv.wait(lk, [&] { return checks_left == 0 || err != FKD_OK; });
+        return err == FKD_OK && host_bad == kNoBad;
+    }
+};
+
+std::vector<int64_t> chunk_schedule(const Knobs& kn, int64_t total, int64_t full_chunk) {
+    std::vector<int64_t> sizes;
+    auto uniform = [&] {
+        for (int64_t b = 0; b < total; b += full_chunk) sizes.push_back(std::min(full_chunk, total - b));
+        return sizes;
+    };
+    if (kn.chunk > 0 || total <= 2 * full_chunk) return uniform();
+    // head ramp full/2^h .. full/2, tail ramp full/2 .. full/2^t
+    std::vector<int64_t> head, tail;
+    for (int j = kn.ramp_head; j >= 1; --j) head.push_back(std::max<int64_t>(1024, full_chunk >> j));
+    for (int j = 1; j <= kn.ramp_tail; ++j) tail.push_back(std::max<int64_t>(1024, full_chunk >> j));
+    int64_t left = total;
+    for (int64_t v : head) left -= v;
+    for (int64_t v : tail) left -= v;
+    if (left < 0) return uniform();  // too short for the ramps
+    sizes = head;
+    while (left > 0) {
+        sizes.push_back(std::min(full_chunk, left));
+        left -= sizes.back();
+    }
+    sizes.insert(sizes.end(), tail.begin(), tail.end());
+    return sizes;
+}
+
+}  // namespace
+}  // namespace fkd
+
 fkd_status fkd_run_batch(const fkd_tree* t, const float* queries, int64_t m, int32_t dim,
                          const fkd_batch_options* o, int32_t* counts, fkd_hit* hits,
                          fkd_query_stats* stats) {
@@ -1037,309 +1264,288 @@ fkd_status fkd_run_batch(const fkd_tree* t, const float* queries, int64_t m, int
     if (stats) *stats = fkd_query_stats{0, 0, 0};
     if (m == 0) return FKD_OK;
     if (t->reps.empty()) return fail(FKD_NO_DEVICE, "tree has no device replica");
+    const Knobs kn = read_knobs();
     const int k = o->kind == FKD_KNN ? o->k : 1;
     const bool want_stats = o->collect_stats != 0;
+    const bool check = t->n > 0;  // require_finite only with a non-empty tree (batch.cpp:75)
     const int ndev = int(t->reps.size());
     const int64_t per_dev = (m + ndev - 1) / ndev;
-    // Chunking: a graduated schedule per device shard — small first chunks
-    // (the first H2D + walk cannot overlap anything), full-size middle
-    // chunks (shard/8), small last chunks (the last D2H cannot overlap
-    // anything) — and four slots (workspaces) per device so the H2D engine,
-    // the SMs and the D2H engine stay busy at once.  FKD_CHUNK fixes a
-    // uniform size; FKD_CHUNK_DIV / FKD_STREAMS are experiment knobs.
-    const char* chunk_env = std::getenv("FKD_CHUNK");
-    const int64_t chunk_div = [] {
-        const char* e = std::getenv("FKD_CHUNK_DIV");
-        return e ? std::max(1, std::atoi(e)) : 8;
-    }();
-    const int n_streams = [] {  // measured (decoupled copy streams): 4 slots beat 6 by ~5% on C3 kNN8 e2e
-        const char* e = std::getenv("FKD_STREAMS");
-        return e ? std::max(1, std::atoi(e)) : 4;
-    }();
-    // ramp depths (FKD_RAMP_HEAD / FKD_RAMP_TAIL: experiment knobs)
-    const int ramp_head = [] {
-        const char* e = std::getenv("FKD_RAMP_HEAD");
-        return e ? std::max(0, std::min(6, std::atoi(e))) : 2;
-    }();
-    const int ramp_tail = [] {
-        const char* e = std::getenv("FKD_RAMP_TAIL");
-        return e ? std::max(0, std::min(6, std::atoi(e))) : 2;
-    }();
-    const int64_t full_chunk = chunk_env
-        ? std::max<int64_t>(1024, std::atoll(chunk_env))
-        : std::min<int64_t>(int64_t(4) << 20,
-                            std::max<int64_t>(int64_t(256) << 10, (per_dev + chunk_div - 1) / chunk_div));
-    auto schedule = [&](int64_t total) {
-        std::vector<int64_t> sizes;
-        if (chunk_env || total <= 2 * full_chunk) {
-            for (int64_t b = 0; b < total; b += full_chunk) sizes.push_back(std::min(full_chunk, total - b));
-            return sizes;
-        }
-        // head ramp full/2^h .. full/2, tail ramp full/2 .. full/2^t
-        std::vector<int64_t> head, tail;
-        for (int j = ramp_head; j >= 1; --j) head.push_back(std::max<int64_t>(1024, full_chunk >> j));
-        for (int j = 1; j <= ramp_tail; ++j) tail.push_back(std::max<int64_t>(1024, full_chunk >> j));
-        int64_t left = total;
-        for (int64_t v : head) left -= v;
-        for (int64_t v : tail) left -= v;
-        if (left < 0) {  // too short for the ramps: uniform chunks
-            for (int64_t b = 0; b < total; b += full_chunk) sizes.push_back(std::min(full_chunk, total - b));
-            return sizes;
-        }
-        sizes = head;
-        while (left > 0) {
-            sizes.push_back(std::min(full_chunk, left));
-            left -= sizes.back();
-        }
-        sizes.insert(sizes.end(), tail.begin(), tail.end());
-        return sizes;
-    };
+    const int64_t full_chunk = kn.chunk > 0 ? kn.chunk
+                                            : std::min<int64_t>(int64_t(4) << 20,
+                                                                std::max<int64_t>(int64_t(256) << 10,
+                                                                                  (per_dev + kn.chunk_div - 1) / kn.chunk_div));
+    const bool want_pg_q = kn.pageable_staging && is_pageable(queries);
+    const bool want_pg_out = kn.pageable_staging && (is_pageable(counts) || is_pageable(hits));
 
-    struct Job {
-        int rep;
-        Workspace* w;
-        int64_t base, count;
-        int64_t off;  // offset in the device's shard (full staging)
-    };
-    std::vector<Job> jobs;
-    std::vector<std::vector<Workspace*>> wss(ndev);
+    std::vector<std::unique_ptr<DevicePipe>> pipes;
+    PipeShared sh;
     fkd_status err = FKD_OK;
+    // ---- plan: shards, chunks, slots, device staging, host rings, events
     for (int di = 0; di < ndev && err == FKD_OK; ++di) {
         const int64_t lo = std::min<int64_t>(m, di * per_dev), hi = std::min<int64_t>(m, lo + per_dev);
         if (hi <= lo) continue;
-        const std::vector<int64_t> sizes = schedule(hi - lo);
-        const int nws = int(std::min<size_t>(sizes.size(), size_t(n_streams)));
+        auto P = std::make_unique<DevicePipe>();
+        P->di = di;
+        P->rep = t->reps[di];
+        DeviceGuard g(P->rep->device);
+        const std::vector<int64_t> sizes = chunk_schedule(kn, hi - lo, full_chunk);
+        const int nws = int(std::min<size_t>(sizes.size(), size_t(kn.streams)));
         for (int j = 0; j < nws && err == FKD_OK; ++j) {
             Workspace* w = nullptr;
-            err = acquire_ws(*t->reps[di], &w);
-            if (err == FKD_OK) wss[di].push_back(w);
+            err = acquire_ws(*P->rep, &w);
+            if (err == FKD_OK) P->wss.push_back(w);
         }
-        // the workspace that already holds the largest staging serves as slot 0
-        // (the pool hands workspaces out in no particular order)
-        std::stable_sort(wss[di].begin(), wss[di].end(),
-                         [](const Workspace* x, const Workspace* y) { return x->h_cap > y->h_cap; });
-        int64_t b = lo;
-        for (size_t c = 0; c < sizes.size() && err == FKD_OK; ++c) {
-            jobs.push_back(Job{di, wss[di][c % wss[di].size()], b, sizes[c], b - lo});
-            b += sizes[c];
-        }
-    }
-    // Staging.  Full (default when it fits in a quarter of the free device
-    // memory): the first slot holds the whole shard's queries and results,
-    // every H2D is issued up front (so the copy-in finishes early instead of
-    // sharing the PCIe link with the copy-out: each direction drops from 55 to
-    // 44 GB/s when both run) and no chunk waits for a slot's buffers.  Ring
-    // (fallback): every slot holds its largest chunk and chunk c reuses slot
-    // c mod R's buffers after chunk c-R's walk / D2H.
-    std::vector<char> full(ndev, 0);
-    if (err == FKD_OK) {
-        const int full_env = [] {  // experiment knob: FKD_FULL_STAGING=0 forces the ring
-            const char* e = std::getenv("FKD_FULL_STAGING");
-            return e ? std::atoi(e) : 1;
-        }();
-        for (int di = 0; di < ndev && err == FKD_OK; ++di) {
-            if (wss[di].empty()) continue;
-            DeviceGuard g(t->reps[di]->device);
-            int64_t shard = 0;
-            for (const Job& j : jobs)
-                if (j.rep == di) shard += j.count;
-            Workspace* w0 = wss[di][0];
-            const int64_t have = std::min({w0->q_cap / std::max(1, dim), w0->c_cap, w0->h_cap / k});
-            bool fits = have >= shard;
-            if (!fits && full_env != 0) {
-                size_t free_b = 0, total_b = 0;
-                cudaMemGetInfo(&free_b, &total_b);
-                fits = double(shard) * (double(dim) * 4 + 4 + 8.0 * k) <= 0.25 * double(free_b);
-            }
-            full[di] = full_env != 0 && fits;
-            for (Workspace* w : wss[di]) {
-                int64_t big = 0;
-                for (const Job& j : jobs)
-                    if (j.w == w) big = std::max(big, j.count);
-                if (full[di]) big = w == w0 ? shard : 0;
-                cudaError_t e = grow(w->q, w->q_cap, big * dim);
-                if (e == cudaSuccess) e = grow(w->counts, w->c_cap, big);
-                if (e == cudaSuccess) e = grow(w->hits, w->h_cap, big * k);
-                if (e != cudaSuccess) err = fail(FKD_CUDA_ERROR, std::string("staging: ") + cudaGetErrorString(e));
-            }
-        }
-    }
-    // FKD_PIPE_TRACE=1: per-chunk H2D start/end, walk end, D2H end on stderr
-    // (development aid; timing events on every stream)
-    const bool trace = std::getenv("FKD_PIPE_TRACE") != nullptr && ndev == 1;
-    // the first chunk's walk gates the first D2H: a smaller step budget ends
-    // its slowest warps sooner (the overflow pass finishes those queries)
-    const int first_div = [] {
-        const char* e = std::getenv("FKD_FIRST_BUDGET_DIV");
-        return e ? std::max(1, std::atoi(e)) : 1;
-    }();
-    const bool tail_prio = [] {  // experiment knob: FKD_TAIL_PRIO=0 keeps the tails on the slot stream
-        const char* e = std::getenv("FKD_TAIL_PRIO");
-        return !e || std::atoi(e) != 0;
-    }();
-    std::vector<cudaEvent_t> tev(trace ? jobs.size() * 4 : 0);
-    for (auto& e : tev) cudaEventCreate(&e);
-    // Pageable caller buffers go through pinned staging (see CopyPool): the
-    // queries of chunk c are copied in by the host just before chunk c is
-    // enqueued; results land in the staging and are copied out chunk by
-    // chunk as each chunk's D2H completes.  FKD_PAGEABLE_STAGING=0 hands
-    // pageable pointers to cudaMemcpyAsync directly (A/B knob).
-    const bool stage_env = [] {
-        const char* e = std::getenv("FKD_PAGEABLE_STAGING");
-        return !e || std::atoi(e) != 0;
-    }();
-    const bool pg_q = stage_env && is_pageable(queries);
-    const bool pg_out = stage_env && (is_pageable(counts) || is_pageable(hits));
-    HostStage hst{};
-    const float* src_q = queries;
-    int32_t* dst_c = counts;
-    fkd_hit* dst_h = hits;
-    std::vector<cudaEvent_t> done(pg_out ? jobs.size() : 0, nullptr);
-    if (err == FKD_OK && (pg_q || pg_out)) {
-        const size_t qb = pg_q ? size_t(m) * dim * sizeof(float) : 0;
-        const size_t cb = pg_out ? size_t(m) * sizeof(int32_t) : 0;
-        const size_t hb = pg_out ? size_t(m) * k * sizeof(fkd_hit) : 0;
-        cudaError_t e = acquire_stage(qb + cb + hb, &hst);
-        if (e != cudaSuccess) err = fail(FKD_CUDA_ERROR, std::string("host staging: ") + cudaGetErrorString(e));
-        if (pg_q) src_q = reinterpret_cast<const float*>(hst.p);
-        if (pg_out) {
-            dst_c = reinterpret_cast<int32_t*>(hst.p + qb);
-            dst_h = reinterpret_cast<fkd_hit*>(hst.p + qb + cb);
-        }
-        for (size_t ji = 0; ji < done.size() && err == FKD_OK; ++ji) {
-            DeviceGuard g(t->reps[jobs[ji].rep]->device);
-            e = cudaEventCreateWithFlags(&done[ji], cudaEventDisableTiming);
-            if (e != cudaSuccess) err = fail(FKD_CUDA_ERROR, std::string("event: ") + cudaGetErrorString(e));
-        }
-    }
-    // Enqueue, per chunk c on slot s = c mod R (a slot = one workspace: its
-    // staging buffers and its compute stream):
-    //   copy-in stream : wait walk(c-R) [slot's q is free] ; H2D ; record in(s)
-    //   slot stream    : wait in(s), wait out(c-R) [slot's results are free] ;
-    //                    order + walk ; record walk(s)
-    //   copy-out stream: wait walk(s) ; D2H counts + hits ; record out(s)
-    // (the two bracketed waits exist only with ring staging).  One H2D and one D2H stream per device keep both copy engines streaming
-    // in chunk order without queueing an H2D behind an unrelated D2H (which
-    // a per-slot H2D -> walk -> D2H stream would), and the walks of
-    // neighbouring chunks overlap each other's tails on the slot streams.
-    // Every wait names an event recorded earlier in host order.  Bad ids
-    // (offset by the chunk base) and stat totals accumulate on the device per
-    // slot and are read once at the end; nothing blocks the host until the
-    // final synchronisation (with pinned caller buffers).
-    for (int di = 0; di < ndev && err == FKD_OK; ++di) {
-        DeviceGuard g(t->reps[di]->device);
-        for (Workspace* w : wss[di]) {
-            cudaError_t e = reset_small(w, w->stream);
-            if (e != cudaSuccess) err = fail(FKD_CUDA_ERROR, std::string("reset: ") + cudaGetErrorString(e));
-        }
-    }
-    for (size_t ji = 0; ji < jobs.size() && err == FKD_OK; ++ji) {
-        const Job& j = jobs[ji];
-        Replica& r = *t->reps[j.rep];
-        DeviceGuard g(r.device);
-        Workspace* w = j.w;
-        Workspace* io = wss[j.rep][0];
-        const bool ring = !full[j.rep];
-        const bool reused = ring && std::count_if(jobs.begin(), jobs.begin() + ji,
-                                                  [&](const Job& x) { return x.w == w; }) > 0;
-        float* dq = ring ? w->q : io->q + j.off * dim;
-        int32_t* dc = ring ? w->counts : io->counts + j.off;
-        fkd_hit* dh = ring ? w->hits : io->hits + j.off * k;
-        int launches = 0, wl = 0;
-        auto tr = [&](int which, cudaStream_t sst) {
-            if (trace) cudaEventRecord(tev[ji * 4 + which], sst);
-        };
-        auto step = [&]() -> fkd_status {
-            if (reused) FKD_CUDA(cudaStreamWaitEvent(io->cin, w->pe[1], 0));
-            tr(0, io->cin);
-            if (pg_q)
-                par_copy(const_cast<float*>(src_q) + j.base * dim, queries + j.base * dim,
-                         size_t(j.count) * dim * sizeof(float));
-            FKD_CUDA(cudaMemcpyAsync(dq, src_q + j.base * dim, size_t(j.count) * dim * sizeof(float),
-                                     cudaMemcpyHostToDevice, io->cin));
-            FKD_CUDA(cudaEventRecord(w->pe[0], io->cin));
-            tr(1, io->cin);
-            FKD_CUDA(cudaStreamWaitEvent(w->stream, w->pe[0], 0));
-            if (reused) FKD_CUDA(cudaStreamWaitEvent(w->stream, w->pe[2], 0));
-            fkd_status e = enqueue(t, r, w, dq, j.count, o, cap2, dc, dh, nullptr,
-                                   want_stats, w->stream, &launches, &wl, nullptr, nullptr, j.base,
-                                   tail_prio ? w->tail : nullptr, ji == 0 ? first_div : 1);
-            if (e != FKD_OK) return e;
-            FKD_CUDA(cudaEventRecord(w->pe[1], w->stream));
-            tr(2, w->stream);
-            FKD_CUDA(cudaStreamWaitEvent(io->cout, w->pe[1], 0));
-            FKD_CUDA(cudaMemcpyAsync(dst_c + j.base, dc, size_t(j.count) * sizeof(int32_t),
-                                     cudaMemcpyDeviceToHost, io->cout));
-            FKD_CUDA(cudaMemcpyAsync(dst_h + j.base * k, dh, size_t(j.count) * k * sizeof(fkd_hit),
-                                     cudaMemcpyDeviceToHost, io->cout));
-            FKD_CUDA(cudaEventRecord(w->pe[2], io->cout));
-            if (pg_out) FKD_CUDA(cudaEventRecord(done[ji], io->cout));
-            tr(3, io->cout);
-            return FKD_OK;
-        };
-        err = step();
-    }
-    for (int di = 0; di < ndev && err == FKD_OK; ++di) {
-        DeviceGuard g(t->reps[di]->device);
-        for (Workspace* w : wss[di]) {
-            cudaError_t e = cudaMemcpyAsync(w->h_small, w->small, 8 * sizeof(unsigned long long),
-                                            cudaMemcpyDeviceToHost, w->stream);
-            if (e != cudaSuccess) err = fail(FKD_CUDA_ERROR, std::string("readback: ") + cudaGetErrorString(e));
-        }
-    }
-    // pageable results: copy each chunk out as soon as its D2H has landed
-    // (overlaps the later chunks' DMA); on error, skip to the drain below
-    for (size_t ji = 0; ji < done.size() && err == FKD_OK; ++ji) {
-        const Job& j = jobs[ji];
-        cudaError_t e = cudaEventSynchronize(done[ji]);
-        if (e != cudaSuccess) {
-            err = fail(FKD_CUDA_ERROR, std::string("chunk: ") + cudaGetErrorString(e));
+        if (err != FKD_OK) {
+            for (Workspace* w : P->wss) release_ws(*P->rep, w);
             break;
         }
-        par_copy(counts + j.base, dst_c + j.base, size_t(j.count) * sizeof(int32_t));
-        par_copy(hits + j.base * k, dst_h + j.base * k, size_t(j.count) * k * sizeof(fkd_hit));
-    }
-    if (trace && err == FKD_OK) {
-        for (auto& e : tev) cudaEventSynchronize(e);
-        for (size_t ji = 0; ji < jobs.size(); ++ji) {
-            float a0 = 0, a1 = 0, a2 = 0, a3 = 0;
-            cudaEventElapsedTime(&a0, tev[0], tev[ji * 4 + 0]);
-            cudaEventElapsedTime(&a1, tev[0], tev[ji * 4 + 1]);
-            cudaEventElapsedTime(&a2, tev[0], tev[ji * 4 + 2]);
-            cudaEventElapsedTime(&a3, tev[0], tev[ji * 4 + 3]);
-            std::fprintf(stderr, "chunk %zu n=%lld h2d %.3f-%.3f walk_end %.3f d2h_end %.3f\n", ji,
-                         (long long)jobs[ji].count, a0, a1, a2, a3);
+        // the workspace that already holds the largest staging serves as slot 0
+        std::stable_sort(P->wss.begin(), P->wss.end(),
+                         [](const Workspace* x, const Workspace* y) { return x->h_cap > y->h_cap; });
+        int64_t b = lo;
+        for (size_t c = 0; c < sizes.size(); ++c) {
+            P->jobs.push_back(PipeJob{b, sizes[c], b - lo, int(c % P->wss.size())});
+            P->max_chunk = std::max(P->max_chunk, sizes[c]);
+            b += sizes[c];
         }
+        const int64_t shard = hi - lo;
+        Workspace* w0 = P->wss[0];
+        const int64_t have = std::min({w0->q_cap / std::max(1, dim), w0->c_cap, w0->h_cap / k});
+        bool fits = have >= shard;
+        if (!fits && kn.full_staging) {
+            size_t free_b = 0, total_b = 0;
+            cudaMemGetInfo(&free_b, &total_b);
+            fits = double(shard) * (double(dim) * 4 + 4 + 8.0 * k) <= 0.25 * double(free_b);
+        }
+        P->full = kn.full_staging && fits;
+        for (size_t wi = 0; wi < P->wss.size() && err == FKD_OK; ++wi) {
+            Workspace* w = P->wss[wi];
+            int64_t big = 0;
+            for (const PipeJob& j : P->jobs)
+                if (j.ws == int(wi)) big = std::max(big, j.count);
+            if (P->full) big = wi == 0 ? shard : 0;
+            cudaError_t e = grow(w->q, w->q_cap, big * dim);
+            if (e == cudaSuccess) e = grow(w->counts, w->c_cap, big);
+            if (e == cudaSuccess) e = grow(w->hits, w->h_cap, big * k);
+            if (e != cudaSuccess) err = fail(FKD_CUDA_ERROR, std::string("staging: ") + cudaGetErrorString(e));
+        }
+        // pinned host rings for pageable caller buffers (fall back to direct
+        // pageable copies when pinned memory is not available)
+        const int64_t ring = std::min<int64_t>(kHostRing, int64_t(P->jobs.size()));
+        if (err == FKD_OK && want_pg_q) {
+            P->pg_q = acquire_stage(size_t(ring * P->max_chunk) * dim * sizeof(float), &P->qst) == cudaSuccess;
+            if (!P->pg_q) cudaGetLastError();
+        }
+        if (err == FKD_OK && want_pg_out) {
+            P->r_slot_bytes = (size_t(P->max_chunk) * (sizeof(int32_t) + size_t(k) * sizeof(fkd_hit)) + 255) & ~size_t(255);
+            P->pg_out = acquire_stage(size_t(ring) * P->r_slot_bytes, &P->rst) == cudaSuccess;
+            if (!P->pg_out) cudaGetLastError();
+        }
+        for (auto* v : {&P->ev_in, &P->ev_walk, &P->ev_out}) {
+            v->assign(P->jobs.size(), nullptr);
+            for (auto& e : *v)
+                if (err == FKD_OK && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
+                    err = fail(FKD_CUDA_ERROR, "event create failed");
+        }
+        for (Workspace* w : P->wss) {
+            cudaError_t e = reset_small(w, w->stream);
+            if (e != cudaSuccess && err == FKD_OK) err = fail(FKD_CUDA_ERROR, std::string("reset: ") + cudaGetErrorString(e));
+        }
+        pipes.push_back(std::move(P));
     }
-    for (auto& e : tev) cudaEventDestroy(e);
-    // drain every stream even after an error, then return workspaces
-    unsigned long long bad = kNoBad, tot[3] = {0, 0, 0};
-    for (int di = 0; di < ndev; ++di) {
-        DeviceGuard g(t->reps[di]->device);
-        if (!wss[di].empty()) {
-            for (cudaStream_t cs : {wss[di][0]->cin, wss[di][0]->cout}) {
-                cudaError_t e = cudaStreamSynchronize(cs);
-                if (e != cudaSuccess && err == FKD_OK)
-                    err = fail(FKD_CUDA_ERROR, std::string("stream: ") + cudaGetErrorString(e));
+    // Host check of the queries (require_finite, batch.cpp:79): fused into the
+    // staging copy (pageable queries, full device staging); up front when the
+    // outputs are staged but the queries are not copied by the host, or the
+    // device ring would make the enqueue thread wait on the drain thread.
+    // With pinned outputs and pinned queries only the device checks (the key
+    // pass / scan flags the batch and its walks exit): pinned outputs are then
+    // unspecified on error, as documented in fkd_b200.h.
+    bool any_out = false, fused_all = true;
+    for (auto& P : pipes) {
+        any_out |= P->pg_out;
+        fused_all &= P->pg_q && P->full;
+    }
+    const bool fused = check && any_out && fused_all;
+    if (err == FKD_OK && check && any_out && !fused) {
+        const int64_t f = par_check(queries, m * dim);
+        if (f >= 0) err = fail(FKD_DATA_ERROR, "queries: non-finite coordinate in point " + std::to_string(f / dim));
+    }
+    sh.checks_left = int(pipes.size());
+
+    // ---- per-device enqueue (and drain) threads
+    auto enqueue_pipe = [&](DevicePipe& P) {
+        DeviceGuard g(P.rep->device);
+        Workspace* io = P.wss[0];
+        const int64_t ring = std::min<int64_t>(kHostRing, int64_t(P.jobs.size()));
+        std::vector<int64_t> last_on_ws(P.wss.size(), -1);
+        for (size_t c = 0; c < P.jobs.size() && !sh.stop; ++c) {
+            const PipeJob& j = P.jobs[c];
+            Workspace* w = P.wss[size_t(j.ws)];
+            const int64_t prev = last_on_ws[size_t(j.ws)];
+            last_on_ws[size_t(j.ws)] = int64_t(c);
+            const bool dring = !P.full;
+            float* dq = dring ? w->q : io->q + j.off * dim;
+            int32_t* dc = dring ? w->counts : io->counts + j.off;
+            fkd_hit* dh = dring ? w->hits : io->hits + j.off * k;
+            const float* src = queries + j.base * dim;
+            auto cuda = [&](cudaError_t e, const char* what) {
+                if (e != cudaSuccess) sh.error(FKD_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+                return e == cudaSuccess;
+            };
+            if (P.pg_q) {
+                const int64_t slot = int64_t(c) % ring;
+                if (int64_t(c) >= ring && !cuda(cudaEventSynchronize(P.ev_in[c - size_t(ring)]), "staging")) break;
+                float* stq = reinterpret_cast<float*>(P.qst.p) + slot * P.max_chunk * dim;
+                const int64_t f = par_copy_check(stq, src, j.count * dim);
+                if (check && f >= 0) {  // this and later chunks are not walked
+                    sh.bad((unsigned long long)(j.base + f / dim));
+                    break;
+                }
+                src = stq;
+            }
+            if (dring && prev >= 0 && !cuda(cudaStreamWaitEvent(io->cin, P.ev_walk[size_t(prev)], 0), "wait")) break;
+            if (!cuda(cudaMemcpyAsync(dq, src, size_t(j.count) * dim * sizeof(float), cudaMemcpyHostToDevice, io->cin), "H2D") ||
+                !cuda(cudaEventRecord(P.ev_in[c], io->cin), "event") ||
+                !cuda(cudaStreamWaitEvent(w->stream, P.ev_in[c], 0), "wait"))
+                break;
+            if (dring && prev >= 0) {  // the slot's results buffer: its previous D2H must be enqueued and done
+                if (P.pg_out) {
+                    std::unique_lock<std::mutex> lk(P.mu);
+                    P.cv.wait(lk, [&] { return P.d2h_enqueued > size_t(prev) || sh.stop; });
+                    if (sh.stop) break;
+                }
+                if (!cuda(cudaStreamWaitEvent(w->stream, P.ev_out[size_t(prev)], 0), "wait")) break;
+            }
+            int launches = 0, wl = 0;
+            const fkd_status e = enqueue(t, *P.rep, w, dq, j.count, o, cap2, dc, dh, nullptr, want_stats, w->stream,
+                                         &launches, &wl, kn, nullptr, nullptr, j.base, w->tail,
+                                         c == 0 ? kn.first_budget_div : 1);
+            if (e != FKD_OK) {
+                sh.error(e, g_err);
+                break;
+            }
+            if (!cuda(cudaEventRecord(P.ev_walk[c], w->stream), "event")) break;
+            if (!P.pg_out) {
+                if (!cuda(cudaStreamWaitEvent(io->cout, P.ev_walk[c], 0), "wait") ||
+                    !cuda(cudaMemcpyAsync(counts + j.base, dc, size_t(j.count) * sizeof(int32_t),
+                                          cudaMemcpyDeviceToHost, io->cout), "D2H") ||
+                    !cuda(cudaMemcpyAsync(hits + j.base * k, dh, size_t(j.count) * k * sizeof(fkd_hit),
+                                          cudaMemcpyDeviceToHost, io->cout), "D2H") ||
+                    !cuda(cudaEventRecord(P.ev_out[c], io->cout), "event"))
+                    break;
+            } else {
+                std::lock_guard<std::mutex> lk(P.mu);
+                P.enqueued = c + 1;
+                P.cv.notify_all();
             }
         }
-        for (Workspace* w : wss[di]) {
-            cudaError_t e = cudaStreamSynchronize(w->stream);
-            if (e != cudaSuccess && err == FKD_OK)
-                err = fail(FKD_CUDA_ERROR, std::string("stream: ") + cudaGetErrorString(e));
-            if (err == FKD_OK) finish_small(w, 0, &bad, tot);
-            release_ws(*t->reps[di], w);
+        {
+            std::lock_guard<std::mutex> lk(P.mu);
+            P.enq_done = true;
+            P.cv.notify_all();
         }
+        sh.checks_done();
+    };
+    auto drain_pipe = [&](DevicePipe& P) {
+        DeviceGuard g(P.rep->device);
+        Workspace* io = P.wss[0];
+        const size_t ring = size_t(std::min<int64_t>(kHostRing, int64_t(P.jobs.size())));
+        bool gate = false, ok = false;
+        auto copy_out = [&](size_t c) {
+            const PipeJob& j = P.jobs[c];
+            if (cudaEventSynchronize(P.ev_out[c]) != cudaSuccess) {
+                sh.error(FKD_CUDA_ERROR, "D2H failed");
+                return;
+            }
+            if (!gate) {  // results reach the caller only once every query passed the check
+                ok = fused ? sh.wait_checks() : (sh.err == FKD_OK);
+                gate = true;
+            }
+            if (!ok || sh.stop) return;
+            const char* slot = P.rst.p + (c % ring) * P.r_slot_bytes;
+            par_copy(counts + j.base, slot, size_t(j.count) * sizeof(int32_t));
+            par_copy(hits + j.base * k, slot + size_t(P.max_chunk) * sizeof(int32_t),
+                     size_t(j.count) * k * sizeof(fkd_hit));
+        };
+        size_t c = 0;
+        for (;; ++c) {
+            {
+                std::unique_lock<std::mutex> lk(P.mu);
+                P.cv.wait(lk, [&] { return P.enqueued > c || P.enq_done; });
+                if (P.enqueued <= c) break;
+            }
+            if (c >= ring) copy_out(c - ring);
+            const PipeJob& j = P.jobs[c];
+            Workspace* w = P.wss[size_t(j.ws)];
+            const int64_t off = P.full ? j.off : 0;
+            const int32_t* dc = P.full ? io->counts + off : w->counts;
+            const fkd_hit* dh = P.full ? io->hits + off * k : w->hits;
+            char* slot = P.rst.p + (c % ring) * P.r_slot_bytes;
+            bool good = cudaStreamWaitEvent(io->cout, P.ev_walk[c], 0) == cudaSuccess &&
+                        cudaMemcpyAsync(slot, dc, size_t(j.count) * sizeof(int32_t), cudaMemcpyDeviceToHost,
+                                        io->cout) == cudaSuccess &&
+                        cudaMemcpyAsync(slot + size_t(P.max_chunk) * sizeof(int32_t), dh,
+                                        size_t(j.count) * k * sizeof(fkd_hit), cudaMemcpyDeviceToHost,
+                                        io->cout) == cudaSuccess &&
+                        cudaEventRecord(P.ev_out[c], io->cout) == cudaSuccess;
+            {
+                std::lock_guard<std::mutex> lk(P.mu);
+                P.d2h_enqueued = c + 1;
+                P.cv.notify_all();
+            }
+            if (!good) {
+                sh.error(FKD_CUDA_ERROR, "D2H enqueue failed");
+                ++c;
+                break;
+            }
+        }
+        for (size_t cc = c > ring ? c - ring : 0; cc < c; ++cc) copy_out(cc);
+    };
+    if (err == FKD_OK) {
+        std::vector<std::thread> threads;
+        // one enqueue thread per device (the caller's thread serves the last
+        // one) and a drain thread per device with staged outputs
+        for (auto& P : pipes)
+            if (P->pg_out) threads.emplace_back(drain_pipe, std::ref(*P));
+        for (size_t i = 0; i + 1 < pipes.size(); ++i) threads.emplace_back(enqueue_pipe, std::ref(*pipes[i]));
+        if (!pipes.empty()) enqueue_pipe(*pipes.back());
+        for (auto& th : threads) th.join();
+        if (sh.err != FKD_OK) err = fail(sh.err, sh.msg);
     }
-    for (auto& e : done)
-        if (e) cudaEventDestroy(e);
-    release_stage(hst);  // every stream that used it is drained
+    // ---- drain every stream, read the device flags and totals, release
+    unsigned long long bad = kNoBad, tot[3] = {0, 0, 0};
+    for (auto& P : pipes) {
+        DeviceGuard g(P->rep->device);
+        for (Workspace* w : P->wss) {
+            cudaError_t e = cudaMemcpyAsync(w->h_small, w->small, 8 * sizeof(unsigned long long),
+                                            cudaMemcpyDeviceToHost, w->stream);
+            if (e != cudaSuccess && err == FKD_OK) err = fail(FKD_CUDA_ERROR, std::string("readback: ") + cudaGetErrorString(e));
+        }
+        for (cudaStream_t cs : {P->wss[0]->cin, P->wss[0]->cout}) {
+            cudaError_t e = cudaStreamSynchronize(cs);
+            if (e != cudaSuccess && err == FKD_OK) err = fail(FKD_CUDA_ERROR, std::string("stream: ") + cudaGetErrorString(e));
+        }
+        for (Workspace* w : P->wss) {
+            cudaError_t e = cudaStreamSynchronize(w->stream);
+            if (e != cudaSuccess && err == FKD_OK) err = fail(FKD_CUDA_ERROR, std::string("stream: ") + cudaGetErrorString(e));
+            if (err == FKD_OK) finish_small(w, 0, &bad, tot);
+            release_ws(*P->rep, w);
+        }
+        for (auto* v : {&P->ev_in, &P->ev_walk, &P->ev_out})
+            for (auto& e : *v)
+                if (e) cudaEventDestroy(e);
+        release_stage(P->qst);  // every stream that used them is drained
+        release_stage(P->rst);
+    }
     if (err != FKD_OK) return err;
+    bad = std::min(bad, sh.host_bad);
     if (bad != kNoBad)
         return fail(FKD_DATA_ERROR, "queries: non-finite coordinate in point " + std::to_string(bad));
     if (stats) *stats = fkd_query_stats{int64_t(tot[0]), int64_t(tot[1]), int64_t(tot[2])};
     return FKD_OK;
 }
+
+extern "C" {
 
 fkd_status fkd_trace_batch(const fkd_tree* t, const float* queries, int32_t m, int32_t dim,
                            int32_t kind, int32_t k, float max_radius, int32_t* counts, fkd_hit* hits,

@@ -193,19 +193,14 @@ fkd_status fkd_tree_load(const char* path, const int32_t* devices, int32_t ndev,
     if (s == FKD_OK) s = fkd_tree_create_device(d, n, dim, nullptr, out);
     cudaFree(d);
     cudaSetDevice(prev);
+    // the other devices get their replicas device to device from the first
+    // (fkd_tree_add_replicas: pipelined fan-out), not from the file again
     if (s == FKD_OK && devices && ndev > 1) {
-        // replicate through the host-path constructor for the other devices
-        fkd_tree_destroy(*out);
-        *out = nullptr;
-        std::vector<float> host(size_t(n) * dim);
-        float* dd = nullptr;
-        cudaSetDevice(dev);
-        cudaMalloc(&dd, host.size() * sizeof(float));
-        s = fkd_read_file_device(path, 1, dd, n, &n, &dim, nullptr);
-        if (s == FKD_OK) cudaMemcpy(host.data(), dd, host.size() * sizeof(float), cudaMemcpyDeviceToHost);
-        cudaFree(dd);
-        cudaSetDevice(prev);
-        if (s == FKD_OK) s = fkd_tree_create(host.data(), n, dim, devices, ndev, out);
+        s = fkd_tree_add_replicas(*out, devices + 1, ndev - 1);
+        if (s != FKD_OK) {
+            fkd_tree_destroy(*out);
+            *out = nullptr;
+        }
     }
     return s;
 }

@@ -96,16 +96,14 @@ int64_t key_bins(int dim) { return int64_t(1) << (morton_bits_per_dim(dim) * dim
 // Counting sort from 2^20 (below, scanning the bins dominates) to 2^25
 // queries (above, the rank atomics are L2-atomic-throughput bound: 1B
 // uniform queries order in 68 ms this way against 32 ms for the onesweep).
+#ifndef FKD_COUNT_SORT_MIN
+#define FKD_COUNT_SORT_MIN (int64_t(1) << 20)
+#endif
+#ifndef FKD_COUNT_SORT_MAX
+#define FKD_COUNT_SORT_MAX (int64_t(1) << 25)
+#endif
 bool use_counting(int64_t m, int dim) {
-    static const int64_t min_m = [] {  // experiment knob: 0 = never
-        const char* e = std::getenv("FKD_COUNT_SORT_MIN");
-        return e ? std::atoll(e) : int64_t(1) << 20;
-    }();
-    static const int64_t max_m = [] {
-        const char* e = std::getenv("FKD_COUNT_SORT_MAX");
-        return e ? std::atoll(e) : int64_t(1) << 25;
-    }();
-    return min_m > 0 && m >= min_m && m <= max_m && dim >= 1 && dim <= 8;
+    return m >= FKD_COUNT_SORT_MIN && m <= FKD_COUNT_SORT_MAX && dim >= 1 && dim <= 8;
 }
 size_t scan_bytes(int64_t bins) {
     size_t bytes = 0;

@@ -578,3 +578,89 @@ def test_slot_list_walk_high_dim(oracle, budget, resume_min, resume_trips, round
                 fast = fk.run_batch(tree, qs, fk.BatchOptions(kind=fk.QueryKind.knn, k=k, max_radius=r))
                 assert np.array_equal(fast.counts, ref[0]) and fast.hits.tobytes() == ref[1].tobytes(), \
                     f"budgeted n={n} k={k} r={r} budget={budget}"
+
+
+def test_rejected_batch_writes_no_output(oracle, monkeypatch):
+    """A non-finite query rejects the batch before any slot is written, as
+    the reference throws before its BatchResult exists (batch.cpp:79 before
+    :82-86): device outputs (key pass / scan flag + walk-entry exit) and
+    pageable host outputs (host check fused into the staging copy, or up front)
+    keep their previous bytes; the reported id is the first bad query."""
+    import ctypes as C
+    import torch
+
+    monkeypatch.setenv("FKD_CHUNK_DIV", "16")
+    pts = fk.clustered_points(8, 1, 40_000, 3)
+    nodes = oracle.build_tree(pts)
+    qs = fk.clustered_points(8, 2, 600_001, 3)
+    qs[512_345, 1] = np.nan
+    qs[590_000, 0] = np.inf
+    for devices in ([0], [0, 0]):
+        tree = fk.KdTree.from_level_order(nodes, devices=devices)
+        for kind, k in ((fk.QueryKind.fcp, 1), (fk.QueryKind.knn, 8)):
+            opts = fk.BatchOptions(kind=kind, k=k)
+            # pageable in, pageable out (fused host check)
+            counts = np.full(len(qs), -7, np.int32)
+            hits = np.full(len(qs) * k, -7, np.int64)
+            o = opts.to_c()
+            rc = fk.LIB.fkd_run_batch(tree.handle, qs.ctypes.data, len(qs), 3, C.byref(o), counts.ctypes.data,
+                                      hits.ctypes.data, None)
+            assert rc == 2 and "non-finite coordinate in point 512345" in fk.LIB.fkd_last_error().decode()
+            assert (counts == -7).all() and (hits == -7).all()
+            # pinned in, pageable out (up-front host check)
+            hq = fk.LIB.fkd_host_alloc(qs.nbytes)
+            C.memmove(hq, qs.ctypes.data, qs.nbytes)
+            rc = fk.LIB.fkd_run_batch(tree.handle, C.c_void_p(hq), len(qs), 3, C.byref(o), counts.ctypes.data,
+                                      hits.ctypes.data, None)
+            fk.LIB.fkd_host_free(hq)
+            assert rc == 2 and "point 512345" in fk.LIB.fkd_last_error().decode()
+            assert (counts == -7).all() and (hits == -7).all()
+        # device-resident batch (Morton key pass and the unsorted scan)
+        dq = torch.from_numpy(qs).cuda()
+        for morton in (True, False):
+            c = torch.full((len(qs),), -7, dtype=torch.int32, device="cuda")
+            h = torch.full((len(qs) * 8,), -7, dtype=torch.int64, device="cuda")
+            with pytest.raises(fk.DataError, match="point 512345"):
+                fk.run_batch_device(tree, dq, c, h, fk.BatchOptions(kind=fk.QueryKind.knn, k=8, morton=morton))
+            assert (c == -7).all().item() and (h == -7).all().item()
+
+
+def test_add_replicas_fanout(oracle):
+    """fkd_tree_add_replicas (pipelined device-to-device chain) gives
+    byte-identical replicas: a batch sharded over them equals the one-replica
+    batch, through both host-buffer modes."""
+    pts = oracle.random_points(21, 70_000, 4)
+    nodes = oracle.build_tree(pts)
+    qs = oracle.random_points(22, 90_001, 4)
+    one = fk.KdTree.from_level_order(nodes, devices=[0])
+    many = fk.KdTree.from_level_order(nodes, devices=[0])
+    many.add_replicas([0, 0, 0])
+    assert many.replica_devices() == [0, 0, 0, 0]
+    for kind, k in ((fk.QueryKind.fcp, 1), (fk.QueryKind.knn, 16)):
+        opt = fk.BatchOptions(kind=kind, k=k, collect_stats=True)
+        a, b = fk.run_batch(one, qs, opt), fk.run_batch(many, qs, opt)
+        assert a.hits.tobytes() == b.hits.tobytes() and np.array_equal(a.counts, b.counts)
+        assert a.stats == b.stats
+
+
+def test_run_batch_device_rejects_bad_tensors(oracle):
+    import torch
+
+    tree = fk.KdTree.from_level_order(oracle.build_tree(oracle.random_points(31, 1000, 3)))
+    q = torch.rand(100, 3, device="cuda")
+    c = torch.empty(100, dtype=torch.int32, device="cuda")
+    h = torch.empty(100 * 8, dtype=torch.int64, device="cuda")
+    knn8 = fk.BatchOptions(kind=fk.QueryKind.knn, k=8)
+    with pytest.raises(fk.DataError, match="expected an"):
+        fk.run_batch_device(tree, q.reshape(-1), c, h, knn8)
+    with pytest.raises(fk.DataError, match="contiguous"):
+        fk.run_batch_device(tree, torch.rand(3, 100, device="cuda").t(), c, h, knn8)
+    with pytest.raises(fk.DataError, match="dtype"):
+        fk.run_batch_device(tree, q.double(), c, h, knn8)
+    with pytest.raises(fk.DataError, match="hits: holds"):
+        fk.run_batch_device(tree, q, c, h[:799], knn8)
+    with pytest.raises(fk.DataError, match="counts"):
+        fk.run_batch_device(tree, q, c.long(), h, knn8)
+    with pytest.raises(fk.DataError, match="CUDA"):
+        fk.run_batch_device(tree, q.cpu(), c, h, knn8)
+    fk.run_batch_device(tree, q, c, h, knn8)  # the well-formed call goes through
