@@ -146,6 +146,30 @@ fkd_status fkd_run_batch_device(const fkd_tree* tree, const float* d_queries, in
                                 fkd_query_stats* d_per_query, void* stream,
                                 fkd_timings* timings);
 
+/* One device-resident batch of fkd_run_batches_device. */
+typedef struct fkd_device_batch {
+    const float* d_queries;      /* m x dim, device                              */
+    int64_t m;
+    int32_t dim;
+    fkd_batch_options opt;
+    int32_t* d_counts;           /* [m], device                                  */
+    fkd_hit* d_hits;             /* [m * stride], device, 8-byte aligned         */
+    fkd_query_stats* stats;      /* host, may be NULL (batch totals)             */
+    fkd_query_stats* d_per_query;/* device, may be NULL                          */
+    fkd_timings* timings;        /* host, may be NULL                            */
+    fkd_status status;           /* out: this batch's status                     */
+} fkd_device_batch;
+
+/* Several independent device-resident batches over the same tree in one
+ * submission: each runs exactly as fkd_run_batch_device would (own
+ * workspace, own result slots, own status), all concurrently on streams
+ * forked from `stream`; the most expensive batch gets the highest stream
+ * priority so the others fill the SMs its tail passes leave idle.  Joins
+ * back into `stream` and synchronises it once.  Returns the first non-OK
+ * status (each batch's is in its `status`). */
+fkd_status fkd_run_batches_device(const fkd_tree* tree, fkd_device_batch* batches, int32_t n,
+                                  void* stream);
+
 /* ---- single-query entry points (traverse.cpp:25-39) ----
  * out_hits holds max(k,1) entries; *out_count receives the number of hits.
  * Validation follows the reference constructors (radius before k). */

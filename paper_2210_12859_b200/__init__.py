@@ -35,13 +35,13 @@ from typing import List, Optional, Sequence
 
 import numpy as np
 
-from ._lib import LIB, LIB_PATH, fkd_batch_options, fkd_query_stats, fkd_timings
+from ._lib import LIB, LIB_PATH, fkd_batch_options, fkd_device_batch, fkd_query_stats, fkd_timings
 
 __all__ = [
     "BatchOptions", "BatchResult", "DataError", "DeviceError", "Engine", "HIT_DTYPE",
     "InvalidArgument", "InvariantError", "KdTree", "QueryKind", "QueryStats", "build_tree",
     "build_level_order", "build_level_order_device", "clustered_points", "fcp", "knn", "random_points", "result_hash", "run_batch",
-    "run_batch_device", "write_query_results", "LIB_PATH",
+    "run_batch_device", "run_batches_device", "write_query_results", "LIB_PATH",
 ]
 
 HIT_DTYPE = np.dtype([("node", "<i4"), ("dist2", "<f4")])  # flatkd::Hit, 8 bytes
@@ -306,18 +306,14 @@ def _stream_ptr(stream):
     return C.c_void_p(int(stream))
 
 
-def run_batch_device(tree: KdTree, queries, counts, hits, options: Optional[BatchOptions] = None,
-                     stream=None, per_query=None, timings: bool = False):
-    """Device-resident batch: torch CUDA tensors in and out, launched on `stream`
-    (default: torch's current stream).  Returns (QueryStats, timings dict|None)."""
+def _check_device_batch(tree: KdTree, queries, counts, hits, options: BatchOptions, per_query=None):
+    """The C ABI takes raw pointers: shapes, dtypes, layout and device are
+    checked here so a wrong tensor raises instead of reading or writing out
+    of bounds.  Returns (m, dim)."""
     import torch
 
-    options = options or BatchOptions()
     if options.kind == QueryKind.knn and options.k < 1:  # batch.cpp:72-73, checked first
         raise InvalidArgument("knn: k must be >= 1")
-    # the C ABI takes raw pointers: shapes, dtypes, layout and device are
-    # checked here so a wrong tensor raises instead of reading or writing
-    # out of bounds
     if queries.dim() != 2:
         raise DataError("queries: expected an (m, dim) tensor")
     m, dim = int(queries.shape[0]), int(queries.shape[1])
@@ -346,8 +342,24 @@ def run_batch_device(tree: KdTree, queries, counts, hits, options: Optional[Batc
     if tree.replica_device() is not None and dev.index != tree.replica_device():
         raise DataError(f"queries are on cuda:{dev.index}, the tree's first replica on "
                         f"cuda:{tree.replica_device()}")
+    return m, dim
+
+
+def _timings_dict(tm: fkd_timings) -> dict:
+    return {"order_ms": tm.order_ms, "walk_ms": tm.walk_ms, "tail_ms": tm.tail_ms, "launches": tm.launches,
+            "walk_launches": tm.walk_launches, "overflowed": tm.overflowed}
+
+
+def run_batch_device(tree: KdTree, queries, counts, hits, options: Optional[BatchOptions] = None,
+                     stream=None, per_query=None, timings: bool = False):
+    """Device-resident batch: torch CUDA tensors in and out, launched on `stream`
+    (default: torch's current stream).  Returns (QueryStats, timings dict|None)."""
+    import torch
+
+    options = options or BatchOptions()
+    m, dim = _check_device_batch(tree, queries, counts, hits, options, per_query)
     if stream is None:
-        stream = torch.cuda.current_stream(dev)
+        stream = torch.cuda.current_stream(queries.device)
     st = fkd_query_stats()
     tm = fkd_timings()
     o = options.to_c()
@@ -357,11 +369,35 @@ def run_batch_device(tree: KdTree, queries, counts, hits, options: Optional[Batc
         C.byref(st) if options.collect_stats else None,
         C.c_void_p(per_query.data_ptr()) if per_query is not None else None,
         _stream_ptr(stream), C.byref(tm) if timings else None))
-    tdict = None
-    if timings:
-        tdict = {"order_ms": tm.order_ms, "walk_ms": tm.walk_ms, "tail_ms": tm.tail_ms, "launches": tm.launches,
-                 "walk_launches": tm.walk_launches, "overflowed": tm.overflowed}
-    return QueryStats.from_c(st), tdict
+    return QueryStats.from_c(st), (_timings_dict(tm) if timings else None)
+
+
+def run_batches_device(tree: KdTree, batches, stream=None, timings: bool = False):
+    """Several independent device batches in one submission
+    (fkd_run_batches_device): ``batches`` is a list of (queries, counts,
+    hits, BatchOptions); each runs exactly as run_batch_device would, all
+    concurrently (the costliest on the highest-priority stream).  Returns a
+    list of (QueryStats, timings dict|None); raises on the first failing batch."""
+    import torch
+
+    n = len(batches)
+    arr = (fkd_device_batch * max(n, 1))()
+    keep = []
+    for i, (q, c, h, opt) in enumerate(batches):
+        opt = opt or BatchOptions()
+        m, dim = _check_device_batch(tree, q, c, h, opt)
+        st, tm = fkd_query_stats(), fkd_timings()
+        keep.append((st, tm, opt))
+        b = arr[i]
+        b.d_queries, b.m, b.dim, b.opt = q.data_ptr(), m, dim, opt.to_c()
+        b.d_counts, b.d_hits = c.data_ptr(), h.data_ptr()
+        b.stats = C.addressof(st) if opt.collect_stats else None
+        b.d_per_query = None
+        b.timings = C.addressof(tm) if timings else None
+    if stream is None and n:
+        stream = torch.cuda.current_stream(batches[0][0].device)
+    _check(LIB.fkd_run_batches_device(tree.handle, arr, n, _stream_ptr(stream)))
+    return [(QueryStats.from_c(st), _timings_dict(tm) if timings else None) for st, tm, _ in keep]
 
 
 def fcp(tree: KdTree, query, max_radius: float = INF, stats: bool = False):

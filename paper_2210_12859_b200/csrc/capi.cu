@@ -83,6 +83,18 @@ const std::vector<int>& round_schedule(const Knobs& kn, int k, int64_t m) {
     return walk_bucket_of(k) <= 4 ? kn.rounds_knn4 : kn.rounds_knn8;
 }
 
+// The store starts node_shift() empty slots into its allocation.  With one
+// slot, siblings 2c+1 / 2c+2 share an aligned pair of slots (for 16-byte
+// nodes: one 32-byte sector) instead of straddling two, so the far child's
+// sector usually arrived with the close child's.  Measured
+// (tools/node_shift_ab.sh, profiles/r01j_node_shift_ab.log): C3 kNN8 walk
+// -1.6%, fcp -1.5%, uniform kNN8 -0.8%, 4-D kNN16 -1%; -DFKD_NODE_SHIFT=0
+// restores the unshifted store.
+#ifndef FKD_NODE_SHIFT
+#define FKD_NODE_SHIFT 1
+#endif
+constexpr int64_t node_shift() { return FKD_NODE_SHIFT; }
+
 // Store layout: padded vectors (1, 4, 4, 4, 8, 8, 8, 8 floats); building with
 // -DFKD_PACKED_LAYOUT=1 keeps 2-D and 3-D nodes at 8 and 12 bytes (SURVEY §7
 // step 3: chosen by measurement).
@@ -503,20 +515,36 @@ bool use_morton(const fkd_tree* t, const fkd_batch_options* o, int64_t m) {
     return t->n > 0 && m > 1 && t->dim <= 8;
 }
 
+// A Morton order computed by another batch of the same submission over the
+// same query array (fkd_run_batches_device): its walk order, the flag its key
+// pass checked the queries into, and the event after which both are ready.
+struct SharedOrder {
+    const uint32_t* order = nullptr;
+    unsigned long long* bad = nullptr;
+    cudaEvent_t ready = nullptr;
+};
+
 // Enqueues one batch (device pointers) on `st`; no synchronisation.  Writes
-// the first bad query id and the stat totals into w->small.
+// the first bad query id and the stat totals into w->small (with a shared
+// order: into the sorting batch's flag).  `ev_sorted`, if given, is recorded
+// once the walk order exists.
 fkd_status enqueue(const fkd_tree* t, Replica& r, Workspace* w, const float* d_q, int64_t m,
                    const fkd_batch_options* o, float cap2, int32_t* d_counts, fkd_hit* d_hits,
                    fkd_query_stats* d_per_query, bool stats, cudaStream_t st, int* launches,
                    int* walk_launches, const Knobs& tu, cudaEvent_t ev_mid, cudaEvent_t ev_tail = nullptr,
-                   int64_t id_offset = 0, cudaStream_t tail_st = nullptr, int budget_div = 1) {
+                   int64_t id_offset = 0, cudaStream_t tail_st = nullptr, int budget_div = 1,
+                   const SharedOrder* share = nullptr, cudaEvent_t ev_sorted = nullptr) {
     const int k = o->kind == FKD_KNN ? o->k : 1;
     if (t->n == 0) {  // every query returns empty; queries are not read (batch.cpp:75)
         *launches += fill_empty(d_counts, d_hits, m, k, st);
         FKD_CUDA(cudaGetLastError());
         return FKD_OK;
     }
-    const bool sort = use_morton(t, o, m);
+    if (share && share->order) {  // ordered (and checked) by the sorting batch
+        FKD_CUDA(cudaStreamWaitEvent(st, share->ready, 0));
+        if (ev_mid) FKD_CUDA(cudaEventRecord(ev_mid, st));
+    }
+    const bool sort = use_morton(t, o, m) && !(share && share->order);
     // sub-batches of <= 2^30 positions: u32 ids in the sort and int32 query ids in the walk
     const int64_t chunk = std::min<int64_t>(m, kSortChunk);
     if (sort) {
@@ -542,7 +570,7 @@ fkd_status enqueue(const fkd_tree* t, Replica& r, Workspace* w, const float* d_q
     // walk writes a slot: the key pass checks each sub-batch it sorts; a batch
     // of several sub-batches, or one walked without the key pass, is scanned
     // first.  The walk kernels exit at entry once *bad is set.
-    if (!sort || m > chunk) {
+    if ((!sort || m > chunk) && !(share && share->order)) {
         *launches += scan_queries(d_q, m, t->dim, w->small, id_offset, st);
         FKD_CUDA(cudaGetLastError());
     }
@@ -590,6 +618,10 @@ fkd_status enqueue(const fkd_tree* t, Replica& r, Workspace* w, const float* d_q
             if (rc < 0) return fail(FKD_CUDA_ERROR, "morton ordering failed");
             *launches += rc;
             a.order = w->ids + half;
+            if (ev_sorted) FKD_CUDA(cudaEventRecord(ev_sorted, st));
+        } else if (share && share->order) {
+            a.order = share->order;
+            a.bad = share->bad;
         }
         if (ev_mid && base == 0) FKD_CUDA(cudaEventRecord(ev_mid, st));
         const bool unordered = (o->flags & FKD_FLAG_UNORDERED) != 0;
@@ -744,17 +776,7 @@ static fkd_status set_frame(fkd_tree* t, const float* lo, const float* hi) {
     return FKD_OK;
 }
 
-// The store starts node_shift() empty slots into its allocation.  With one
-// slot, siblings 2c+1 / 2c+2 share an aligned pair of slots (for 16-byte
-// nodes: one 32-byte sector) instead of straddling two, so the far child's
-// sector usually arrived with the close child's.  Measured
-// (tools/node_shift_ab.sh, profiles/r01j_node_shift_ab.log): C3 kNN8 walk
-// -1.6%, fcp -1.5%, uniform kNN8 -0.8%, 4-D kNN16 -1%; -DFKD_NODE_SHIFT=0
-// restores the unshifted store.
-#ifndef FKD_NODE_SHIFT
-#define FKD_NODE_SHIFT 1
-#endif
-static int64_t node_shift() { return FKD_NODE_SHIFT; }
+
 
 static fkd_status alloc_store(Replica* r, int64_t n, int stride) {
     const int64_t sh = node_shift();
@@ -1086,52 +1108,183 @@ fkd_status fkd_run_batch_device(const fkd_tree* t, const float* d_q, int64_t m, 
                                 const fkd_batch_options* o, int32_t* d_counts, fkd_hit* d_hits,
                                 fkd_query_stats* stats, fkd_query_stats* d_per_query, void* stream,
                                 fkd_timings* timings) {
+    fkd_device_batch b{};
+    b.d_queries = d_q;
+    b.m = m;
+    b.dim = dim;
+    if (o) b.opt = *o;
+    b.d_counts = d_counts;
+    b.d_hits = d_hits;
+    b.stats = stats;
+    b.d_per_query = d_per_query;
+    b.timings = timings;
+    if (!o) return fail(FKD_INVALID_ARGUMENT, "null options");
+    const fkd_status s = fkd_run_batches_device(t, &b, 1, stream);
+    return s;
+}
+
+}  // extern "C"
+
+namespace fkd {
+struct BatchItem {
+    fkd_device_batch* b = nullptr;
     float cap2 = 0.0f;
-    fkd_status s = validate(t, m, dim, o, &cap2);
-    if (s != FKD_OK) return s;
-    if (stats) *stats = fkd_query_stats{0, 0, 0};
-    if (timings) *timings = fkd_timings{0.0f, 0.0f, 0.0f, 0, 0, 0};
-    if (m == 0) return FKD_OK;
-    if (t->reps.empty()) return fail(FKD_NO_DEVICE, "tree has no device replica");
-    if ((reinterpret_cast<uintptr_t>(d_hits) & 7u) != 0)
-        return fail(FKD_INVALID_ARGUMENT, "hits buffer must be 8-byte aligned");
+    Workspace* w = nullptr;
+    cudaStream_t st = nullptr;
+    int launches = 0, walk_launches = 0;
+    bool run = false;
+    double cost = 0.0;
+    unsigned long long* bad_src = nullptr;  // the flag of the batch whose order this one shared
+};
+}  // namespace fkd
+
+extern "C" {
+
+// Several independent batches in one submission (e.g. the fcp and the kNN
+// request of a step, or two clients' batches).  Each runs exactly as
+// fkd_run_batch_device would, with its own workspace, on its own stream
+// forked from the caller's; the most expensive batch (by kind, k and size)
+// gets the highest stream priority, so its blocks are dispatched first and
+// the cheaper batches' walks fill the SMs its straggler warps, continuation
+// rounds and CTA pass leave idle — the one-batch tail phases run at
+// 24-82% of the SMs (profiles/r01k_knn8_kernels.jsonl).  Results, statuses
+// and counters are each batch's own; the call synchronises the caller's
+// stream once, after every batch.
+fkd_status fkd_run_batches_device(const fkd_tree* t, fkd_device_batch* batches, int32_t n, void* stream) {
+    if (n < 0 || (n > 0 && !batches)) return fail(FKD_INVALID_ARGUMENT, "bad batch list");
+    if (!t) return fail(FKD_INVALID_ARGUMENT, "null tree");
+    using Item = BatchItem;
+    std::vector<Item> items(static_cast<size_t>(n));
+    fkd_status first = FKD_OK;
+    std::string first_msg;
+    auto note = [&](fkd_device_batch* b, fkd_status s) {
+        b->status = s;
+        if (s != FKD_OK && first == FKD_OK) {
+            first = s;
+            first_msg = g_err;
+        }
+    };
+    // validation in the reference's order, per batch (batch.cpp:72-80)
+    for (int32_t i = 0; i < n; ++i) {
+        Item& it = items[size_t(i)];
+        it.b = &batches[i];
+        fkd_device_batch* b = it.b;
+        if (b->stats) *b->stats = fkd_query_stats{0, 0, 0};
+        if (b->timings) *b->timings = fkd_timings{0.0f, 0.0f, 0.0f, 0, 0, 0};
+        fkd_status s = validate(t, b->m, b->dim, &b->opt, &it.cap2);
+        if (s == FKD_OK && b->m > 0 && t->reps.empty()) s = fail(FKD_NO_DEVICE, "tree has no device replica");
+        if (s == FKD_OK && b->m > 0 && (reinterpret_cast<uintptr_t>(b->d_hits) & 7u) != 0)
+            s = fail(FKD_INVALID_ARGUMENT, "hits buffer must be 8-byte aligned");
+        note(b, s);
+        it.run = s == FKD_OK && b->m > 0;
+        const int k = b->opt.kind == FKD_KNN ? b->opt.k : 1;
+        it.cost = double(b->m) * (k == 1 ? 1.0 : 2.0 + std::log2(double(k)));
+    }
+    std::vector<Item*> order;
+    for (Item& it : items)
+        if (it.run) order.push_back(&it);
+    if (order.empty()) return first == FKD_OK ? FKD_OK : fail(first, first_msg);
+    std::stable_sort(order.begin(), order.end(), [](const Item* a, const Item* b) { return a->cost > b->cost; });
     Replica& r = *t->reps[0];
     DeviceGuard g(r.device);
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
-    Workspace* w = nullptr;
-    if ((s = acquire_ws(r, &w)) != FKD_OK) return s;
-    const bool want_stats = stats != nullptr || d_per_query != nullptr;
+    cudaStream_t caller = static_cast<cudaStream_t>(stream);
     const Knobs kn = read_knobs();
-    int launches = 0, walk_launches = 0;
-    auto body = [&]() -> fkd_status {
-        FKD_CUDA(reset_small(w, st));
-        if (timings) FKD_CUDA(cudaEventRecord(w->ev[0], st));
-        fkd_status e = enqueue(t, r, w, d_q, m, o, cap2, d_counts, d_hits, d_per_query, want_stats,
-                               st, &launches, &walk_launches, kn, timings ? w->ev[1] : nullptr,
-                               timings ? w->ev[3] : nullptr);
-        if (e != FKD_OK) return e;
-        if (timings) FKD_CUDA(cudaEventRecord(w->ev[2], st));
-        FKD_CUDA(cudaMemcpyAsync(w->h_small, w->small, 8 * sizeof(unsigned long long),
-                                 cudaMemcpyDeviceToHost, st));
-        FKD_CUDA(cudaStreamSynchronize(st));
-        unsigned long long bad = kNoBad, tot[3] = {0, 0, 0};
-        finish_small(w, 0, &bad, tot);
-        if (bad != kNoBad)
-            return fail(FKD_DATA_ERROR, "queries: non-finite coordinate in point " + std::to_string(bad));
-        if (stats) *stats = fkd_query_stats{int64_t(tot[0]), int64_t(tot[1]), int64_t(tot[2])};
-        if (timings) {
-            cudaEventElapsedTime(&timings->order_ms, w->ev[0], w->ev[1]);
-            cudaEventElapsedTime(&timings->walk_ms, w->ev[1], w->ev[2]);
-            cudaEventElapsedTime(&timings->tail_ms, w->ev[3], w->ev[2]);
-            timings->launches = launches;
-            timings->walk_launches = walk_launches;
-            timings->overflowed = int64_t(w->h_small[5]);
-        }
-        return FKD_OK;
+    fkd_status err = FKD_OK;
+    for (Item* it : order) {
+        if (err == FKD_OK) err = acquire_ws(r, &it->w);
+        if (err != FKD_OK) break;
+        // one batch: the caller's stream; several: the costliest on the
+        // workspace's high-priority stream, the others on normal ones
+        it->st = order.size() == 1 ? caller : (it == order.front() ? it->w->tail : it->w->stream);
+    }
+    auto cuda = [&](cudaError_t e, const char* what) {
+        if (e != cudaSuccess && err == FKD_OK) err = fail(FKD_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+        return e == cudaSuccess;
     };
-    s = body();
-    release_ws(r, w);
-    return s;
+    size_t enq = 0;
+    if (err == FKD_OK && order.size() > 1) {  // fork from the caller's stream
+        Workspace* w0 = order.front()->w;
+        if (cuda(cudaEventRecord(w0->pe[0], caller), "fork"))
+            for (Item* it : order) cuda(cudaStreamWaitEvent(it->st, w0->pe[0], 0), "fork");
+    }
+    // Batches over the same query array share one Morton order: the walk
+    // order never changes a result (each query is independent), so sorting
+    // identical queries twice is redundant work.  The first (costliest) such
+    // batch sorts and checks the queries; the others wait for its order.
+    auto sortable = [&](const Item* it) {
+        return use_morton(t, &it->b->opt, it->b->m) && it->b->m <= kSortChunk;
+    };
+    std::vector<SharedOrder> shares(order.size());
+    for (size_t i = 0; i < order.size(); ++i) {
+        Item* it = order[i];
+        if (err != FKD_OK) break;
+        fkd_device_batch* b = it->b;
+        Workspace* w = it->w;
+        cudaStream_t st = it->st;
+        const bool want_stats = b->stats != nullptr || b->d_per_query != nullptr;
+        const SharedOrder* share = nullptr;
+        for (size_t j = 0; j < i && sortable(it); ++j) {
+            const fkd_device_batch* o2 = order[j]->b;
+            if (shares[j].order && o2->d_queries == b->d_queries && o2->m == b->m && o2->dim == b->dim) {
+                share = &shares[j];
+                break;
+            }
+        }
+        if (!cuda(reset_small(w, st), "reset")) break;
+        if (b->timings) cuda(cudaEventRecord(w->ev[0], st), "event");
+        const fkd_status e = enqueue(t, r, w, b->d_queries, b->m, &b->opt, it->cap2, b->d_counts, b->d_hits,
+                                     b->d_per_query, want_stats, st, &it->launches, &it->walk_launches, kn,
+                                     b->timings ? w->ev[1] : nullptr, b->timings ? w->ev[3] : nullptr, 0,
+                                     nullptr, 1, share, (!share && sortable(it)) ? w->pe[2] : nullptr);
+        if (e == FKD_OK && !share && sortable(it) && order.size() > 1)
+            shares[i] = SharedOrder{w->ids + w->key_cap / 2, w->small, w->pe[2]};
+        it->bad_src = share ? share->bad : nullptr;
+        if (e != FKD_OK) {
+            err = e;
+            break;
+        }
+        if (b->timings) cuda(cudaEventRecord(w->ev[2], st), "event");
+        cuda(cudaMemcpyAsync(w->h_small, w->small, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st),
+             "readback");
+        if (order.size() > 1 && cuda(cudaEventRecord(w->pe[1], st), "join")) cuda(cudaStreamWaitEvent(caller, w->pe[1], 0), "join");
+        ++enq;
+    }
+    // one synchronisation for all: the non-finite check must be a status
+    const cudaError_t se = cudaStreamSynchronize(caller);
+    for (Item* it : order)  // (after an error, batches forked but not joined)
+        if (it->w && it->st != caller) cudaStreamSynchronize(it->st);
+    if (se != cudaSuccess && err == FKD_OK) err = fail(FKD_CUDA_ERROR, std::string("batch: ") + cudaGetErrorString(se));
+    for (size_t i = 0; i < order.size(); ++i) {
+        Item* it = order[i];
+        if (!it->w) continue;
+        fkd_device_batch* b = it->b;
+        Workspace* w = it->w;
+        if (err != FKD_OK || i >= enq) {
+            note(b, err != FKD_OK ? err : FKD_CUDA_ERROR);
+        } else {
+            unsigned long long bad = kNoBad, tot[3] = {0, 0, 0};
+            finish_small(w, 0, &bad, tot);
+            if (it->bad_src)  // checked by the batch whose order it shared (same queries)
+                for (Item* o2 : order)
+                    if (o2->w && o2->w->small == it->bad_src) bad = std::min(bad, o2->w->h_small[0]);
+            if (bad != kNoBad) {
+                note(b, fail(FKD_DATA_ERROR, "queries: non-finite coordinate in point " + std::to_string(bad)));
+            } else {
+                if (b->stats) *b->stats = fkd_query_stats{int64_t(tot[0]), int64_t(tot[1]), int64_t(tot[2])};
+                if (b->timings) {
+                    cudaEventElapsedTime(&b->timings->order_ms, w->ev[0], w->ev[1]);
+                    cudaEventElapsedTime(&b->timings->walk_ms, w->ev[1], w->ev[2]);
+                    cudaEventElapsedTime(&b->timings->tail_ms, w->ev[3], w->ev[2]);
+                    b->timings->launches = it->launches;
+                    b->timings->walk_launches = it->walk_launches;
+                    b->timings->overflowed = int64_t(w->h_small[5]);
+                }
+            }
+        }
+        release_ws(r, w);
+    }
+    if (first != FKD_OK) return fail(first, first_msg);
+    return FKD_OK;
 }
 
 }  // extern "C"

@@ -42,16 +42,20 @@ void set_carveout(K kernel) {
         cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, FKD_L1_CARVEOUT);
 }
 
+template <class K>
+void launch_walk_grid(K kernel, const WalkArgs& a, unsigned grid, cudaStream_t st) {
+    set_carveout(kernel);
+    kernel<<<grid, kWalkThreads, 0, st>>>(a);
+}
+
 template <int D, int S, int KB, bool STATS, bool UNORDERED>
 void launch_one(const WalkArgs& a, cudaStream_t st) {
-    set_carveout(walk_kernel<D, S, KB, STATS, UNORDERED>);
-    walk_kernel<D, S, KB, STATS, UNORDERED><<<walk_blocks(a.m, kWalkThreads), kWalkThreads, 0, st>>>(a);
+    launch_walk_grid(walk_kernel<D, S, KB, STATS, UNORDERED>, a, walk_blocks(a.m, kWalkThreads), st);
 }
 
 template <int D, int S, int KB, bool UNORDERED>
 void launch_round(const WalkArgs& a, cudaStream_t st) {
-    set_carveout(walk_round_kernel<D, S, KB, UNORDERED>);
-    walk_round_kernel<D, S, KB, UNORDERED><<<walk_blocks(a.m, kWalkThreads), kWalkThreads, 0, st>>>(a);
+    launch_walk_grid(walk_round_kernel<D, S, KB, UNORDERED>, a, walk_blocks(a.m, kWalkThreads), st);
 }
 
 // phase 0: the walk kernel; phase 1: the overflow pass (when budgeted);

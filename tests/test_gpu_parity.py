@@ -664,3 +664,48 @@ def test_run_batch_device_rejects_bad_tensors(oracle):
     with pytest.raises(fk.DataError, match="CUDA"):
         fk.run_batch_device(tree, q.cpu(), c, h, knn8)
     fk.run_batch_device(tree, q, c, h, knn8)  # the well-formed call goes through
+
+
+def test_run_batches_device_concurrent_exact(oracle):
+    """fkd_run_batches_device: several batches in one submission (forked
+    streams, priorities, one shared Morton order for batches over the same
+    query array) give exactly what separate run_batch_device calls give;
+    statuses are per batch."""
+    import torch
+
+    pts = fk.clustered_points(41, 1, 200_000, 3)
+    tree = fk.KdTree.from_level_order(oracle.build_tree(pts))
+    qa = torch.from_numpy(fk.clustered_points(41, 2, 300_001, 3)).cuda()
+    qb = torch.from_numpy(fk.random_points(41, 3, 120_000, 3)).cuda()
+    specs = [(qa, fk.BatchOptions(kind=fk.QueryKind.fcp)),
+             (qa, fk.BatchOptions(kind=fk.QueryKind.knn, k=8)),
+             (qa, fk.BatchOptions(kind=fk.QueryKind.knn, k=20, max_radius=0.05)),
+             (qa, fk.BatchOptions(kind=fk.QueryKind.knn, k=4, morton=False)),
+             (qb, fk.BatchOptions(kind=fk.QueryKind.knn, k=8, collect_stats=True))]
+    outs = [(torch.full((q.shape[0],), -7, dtype=torch.int32, device="cuda"),
+             torch.full((q.shape[0] * o.stride,), -7, dtype=torch.int64, device="cuda")) for q, o in specs]
+    res = fk.run_batches_device(tree, [(q, c, h, o) for (q, o), (c, h) in zip(specs, outs)], timings=True)
+    for (q, o), (c, h), (st, tm) in zip(specs, outs, res):
+        c2 = torch.empty_like(c)
+        h2 = torch.empty_like(h)
+        st2, _ = fk.run_batch_device(tree, q, c2, h2, o)
+        assert torch.equal(c, c2) and torch.equal(h, h2), o
+        assert tm["walk_launches"] >= 1
+        if o.collect_stats:
+            assert st == st2 and st.nodes_processed > 0
+    # a rejected batch leaves its own slots (and only its own) untouched
+    bad = qa.clone()
+    bad[1234, 2] = float("nan")
+    c_ok, h_ok = torch.empty(qb.shape[0], dtype=torch.int32, device="cuda"), \
+        torch.empty(qb.shape[0] * 8, dtype=torch.int64, device="cuda")
+    c_bad = torch.full((bad.shape[0],), -7, dtype=torch.int32, device="cuda")
+    h_bad = torch.full((bad.shape[0] * 8,), -7, dtype=torch.int64, device="cuda")
+    c_bad2 = torch.full((bad.shape[0],), -7, dtype=torch.int32, device="cuda")
+    with pytest.raises(fk.DataError, match="point 1234"):
+        fk.run_batches_device(tree, [(bad, c_bad, h_bad, fk.BatchOptions(kind=fk.QueryKind.knn, k=8)),
+                                     (bad, c_bad2, torch.empty_like(c_bad2).long(), fk.BatchOptions()),
+                                     (qb, c_ok, h_ok, fk.BatchOptions(kind=fk.QueryKind.knn, k=8))])
+    assert (c_bad == -7).all().item() and (h_bad == -7).all().item() and (c_bad2 == -7).all().item()
+    c_ref, h_ref = torch.empty_like(c_ok), torch.empty_like(h_ok)
+    fk.run_batch_device(tree, qb, c_ref, h_ref, fk.BatchOptions(kind=fk.QueryKind.knn, k=8))
+    assert torch.equal(c_ok, c_ref) and torch.equal(h_ok, h_ref)
