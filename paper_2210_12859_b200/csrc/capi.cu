@@ -366,10 +366,20 @@ std::vector<HostStage> g_stage_pool;
 
 cudaError_t acquire_stage(size_t bytes, HostStage* out) {
     {
+        // best fit: the smallest pooled buffer that holds `bytes`, else the
+        // largest (re-allocated below), so a call's query and result rings
+        // each find their own buffer again on the next call
         std::lock_guard<std::mutex> lk(g_stage_mu);
         auto best = g_stage_pool.end();
-        for (auto it = g_stage_pool.begin(); it != g_stage_pool.end(); ++it)
-            if (best == g_stage_pool.end() || it->cap > best->cap) best = it;
+        for (auto it = g_stage_pool.begin(); it != g_stage_pool.end(); ++it) {
+            if (best == g_stage_pool.end()) {
+                best = it;
+                continue;
+            }
+            const bool fits = it->cap >= bytes, best_fits = best->cap >= bytes;
+            if ((fits && (!best_fits || it->cap < best->cap)) || (!fits && !best_fits && it->cap > best->cap))
+                best = it;
+        }
         if (best != g_stage_pool.end()) {
             *out = *best;
             g_stage_pool.erase(best);
@@ -1322,7 +1332,6 @@ fkd_status fkd_run_batches_device(const fkd_tree* t, fkd_device_batch* batches, 
 namespace fkd {
 namespace {
 
-constexpr int kHostRing = 4;  // pinned staging slots per direction per device
 
 struct PipeJob {
     int64_t base, count, off;  // global query offset, size, offset in the device's shard
@@ -1423,10 +1432,15 @@ fkd_status fkd_run_batch(const fkd_tree* t, const float* queries, int64_t m, int
     const bool check = t->n > 0;  // require_finite only with a non-empty tree (batch.cpp:75)
     const int ndev = int(t->reps.size());
     const int64_t per_dev = (m + ndev - 1) / ndev;
+    // middle chunk = shard / div: 8 for kNN lists (D2H-bound: C3 kNN8 pinned
+    // 15.6 ms vs 16.3 at 4); 4 for one-slot results, whose call is bound by
+    // the chunk walks (C3 fcp pageable 9.4 -> 7.4 ms, pinned 4.7 -> 4.6;
+    // tools/e2e_ab.py, profiles/r02/r02h_e2e_ab.log)
+    const int64_t div = kn.chunk_div > 0 ? kn.chunk_div : (k == 1 ? 4 : 8);
     const int64_t full_chunk = kn.chunk > 0 ? kn.chunk
                                             : std::min<int64_t>(int64_t(4) << 20,
                                                                 std::max<int64_t>(int64_t(256) << 10,
-                                                                                  (per_dev + kn.chunk_div - 1) / kn.chunk_div));
+                                                                                  (per_dev + div - 1) / div));
     const bool want_pg_q = kn.pageable_staging && is_pageable(queries);
     const bool want_pg_out = kn.pageable_staging && (is_pageable(counts) || is_pageable(hits));
 
@@ -1484,7 +1498,7 @@ fkd_status fkd_run_batch(const fkd_tree* t, const float* queries, int64_t m, int
         }
         // pinned host rings for pageable caller buffers (fall back to direct
         // pageable copies when pinned memory is not available)
-        const int64_t ring = std::min<int64_t>(kHostRing, int64_t(P->jobs.size()));
+        const int64_t ring = std::min<int64_t>(kn.host_ring, int64_t(P->jobs.size()));
         if (err == FKD_OK && want_pg_q) {
             P->pg_q = acquire_stage(size_t(ring * P->max_chunk) * dim * sizeof(float), &P->qst) == cudaSuccess;
             if (!P->pg_q) cudaGetLastError();
@@ -1529,7 +1543,7 @@ fkd_status fkd_run_batch(const fkd_tree* t, const float* queries, int64_t m, int
     auto enqueue_pipe = [&](DevicePipe& P) {
         DeviceGuard g(P.rep->device);
         Workspace* io = P.wss[0];
-        const int64_t ring = std::min<int64_t>(kHostRing, int64_t(P.jobs.size()));
+        const int64_t ring = std::min<int64_t>(kn.host_ring, int64_t(P.jobs.size()));
         std::vector<int64_t> last_on_ws(P.wss.size(), -1);
         for (size_t c = 0; c < P.jobs.size() && !sh.stop; ++c) {
             const PipeJob& j = P.jobs[c];
@@ -1602,7 +1616,7 @@ fkd_status fkd_run_batch(const fkd_tree* t, const float* queries, int64_t m, int
     auto drain_pipe = [&](DevicePipe& P) {
         DeviceGuard g(P.rep->device);
         Workspace* io = P.wss[0];
-        const size_t ring = size_t(std::min<int64_t>(kHostRing, int64_t(P.jobs.size())));
+        const size_t ring = size_t(std::min<int64_t>(kn.host_ring, int64_t(P.jobs.size())));
         bool gate = false, ok = false;
         auto copy_out = [&](size_t c) {
             const PipeJob& j = P.jobs[c];

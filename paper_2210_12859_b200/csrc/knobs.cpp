@@ -35,13 +35,14 @@ Knobs read_knobs() {
         k.rounds_knn_all = true;
     }
     if (const char* e = std::getenv("FKD_CHUNK")) k.chunk = std::max<int64_t>(1024, std::atoll(e));
-    if (const char* e = std::getenv("FKD_CHUNK_DIV")) k.chunk_div = std::max(1, std::atoi(e));
+    if (const char* e = std::getenv("FKD_CHUNK_DIV")) k.chunk_div = std::max(0, std::atoi(e));
     if (const char* e = std::getenv("FKD_STREAMS")) k.streams = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("FKD_RAMP_HEAD")) k.ramp_head = std::max(0, std::min(6, std::atoi(e)));
     if (const char* e = std::getenv("FKD_RAMP_TAIL")) k.ramp_tail = std::max(0, std::min(6, std::atoi(e)));
     if (const char* e = std::getenv("FKD_FIRST_BUDGET_DIV")) k.first_budget_div = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("FKD_FULL_STAGING")) k.full_staging = std::atoi(e) != 0;
     if (const char* e = std::getenv("FKD_PAGEABLE_STAGING")) k.pageable_staging = std::atoi(e) != 0;
+    if (const char* e = std::getenv("FKD_HOST_RING")) k.host_ring = std::max(1, std::atoi(e));
     return k;
 }
 

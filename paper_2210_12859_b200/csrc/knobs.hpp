@@ -12,12 +12,13 @@
 //   FKD_RESUME_MIN       parked walks that select the plain-grid resume pass (0: SMs x 64)
 //   FKD_RESUME_TRIPS     trips the resume pass adds before the CTA pass (0: per kind, <0 unbounded)
 //   FKD_CHUNK            host path: uniform chunk size instead of the graduated schedule
-//   FKD_CHUNK_DIV        host path: middle chunk = shard / DIV (8)
+//   FKD_CHUNK_DIV        host path: middle chunk = shard / DIV (0: 4 for k = 1, else 8)
 //   FKD_STREAMS          host path: slot streams per device (4)
 //   FKD_RAMP_HEAD/TAIL   host path: ramp depths of the chunk schedule (2 / 2)
 //   FKD_FIRST_BUDGET_DIV host path: first chunk's budget divisor (1)
 //   FKD_FULL_STAGING     host path: 0 forces the device-side ring staging
 //   FKD_PAGEABLE_STAGING host path: 0 hands pageable caller buffers to cudaMemcpyAsync
+//   FKD_HOST_RING        host path: pinned staging slots per direction per device (4)
 //
 // Experiments that were measured and settled are compile-time constants
 // (store layout, node shift, carveout, Morton bits, sort thresholds, CTA-pass
@@ -43,12 +44,13 @@ struct Knobs {
     int resume_trips = 0;
     // host pipeline
     int64_t chunk = 0;  // 0: graduated schedule
-    int chunk_div = 8;
+    int chunk_div = 0;  // 0: per kind (chunk_div_for)
     int streams = 4;
     int ramp_head = 2, ramp_tail = 2;
     int first_budget_div = 1;
     bool full_staging = true;
     bool pageable_staging = true;
+    int host_ring = 4;
 };
 
 // A snapshot of the environment overrides on top of the defaults.
