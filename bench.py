@@ -393,9 +393,9 @@ def run_b200(args) -> None:
     # queries, the walk and D2H of every result slot inside the timed region.
     # Pinned caller buffers (fkd_host_alloc) -> `e2e`; the drop-in as a
     # reference caller makes it (NumPy / std::vector, pageable) -> `e2e_pageable`.
-    h2d = d2h = 0
+    h2d = m * dim * 4 * (len(batches) if args.serial else 1)  # one upload per step when grouped
+    d2h = 0
     for kind, k, _ in batches:
-        h2d += m * dim * 4
         d2h += m * 4 + m * k * 8
 
     def host_buffers(pinned: bool):
@@ -419,13 +419,26 @@ def run_b200(args) -> None:
     def e2e_run(pinned: bool) -> tuple[float, bool]:
         hq, bufs = host_buffers(pinned)
 
+        arr = (fk._lib.fkd_host_batch * len(batches))()
+        for i, ((kind, k, _), o) in enumerate(zip(batches, opts)):
+            hc, hh = bufs[(kind, k)]
+            arr[i].queries, arr[i].m, arr[i].dim, arr[i].opt = hq, m, dim, o.to_c()
+            arr[i].counts, arr[i].hits, arr[i].stats = hc, hh, None
+
         def e2e_step():
-            for (kind, k, _), o in zip(batches, opts):
-                hc, hh = bufs[(kind, k)]
-                co = o.to_c()
-                rc = fk.LIB.fkd_run_batch(tree.handle, hq, m, dim, C.byref(co), hc, hh, None)
-                if rc != 0:
-                    raise RuntimeError(fk.LIB.fkd_last_error().decode())
+            if args.serial:  # one fkd_run_batch call per batch
+                for (kind, k, _), o in zip(batches, opts):
+                    hc, hh = bufs[(kind, k)]
+                    co = o.to_c()
+                    rc = fk.LIB.fkd_run_batch(tree.handle, hq, m, dim, C.byref(co), hc, hh, None)
+                    if rc != 0:
+                        raise RuntimeError(fk.LIB.fkd_last_error().decode())
+                return
+            # one fkd_run_batches call: the step's batches share the query
+            # array, so they run as one pipeline (one upload per chunk)
+            rc = fk.LIB.fkd_run_batches(tree.handle, arr, len(batches))
+            if rc != 0:
+                raise RuntimeError(fk.LIB.fkd_last_error().decode())
 
         for _ in range(max(1, args.warmup)):
             e2e_step()
@@ -504,7 +517,9 @@ def run_b200(args) -> None:
         "config": workload_config(args.workload, world),
         "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "results_equal_device_path": bool(e2e_parity),
-                "path": "fkd_run_batch (C ABI, pinned host buffers from fkd_host_alloc, chunked H2D/walk/D2H)"},
+                "path": ("fkd_run_batch per batch" if args.serial else "one fkd_run_batches call per step (the "
+                         "batches share the query array: one chunked pipeline, one upload)") +
+                        " (C ABI, pinned host buffers from fkd_host_alloc, chunked H2D/walk/D2H)"},
         "gpu_launches": launches // args.steps,
         "gpu_launches_note": "own kernels per timed step (per batch: Morton keys, walk, continuation "
                              "rounds (fcp: 3), resume pass, CTA overflow pass); CUB sort kernels excluded",
@@ -537,7 +552,7 @@ def run_b200(args) -> None:
     if e2e_pg_value is not None:
         line["e2e_pageable"] = {"value": e2e_pg_value, "unit": "queries/s", "h2d_bytes_per_step": h2d,
                                 "d2h_bytes_per_step": d2h, "results_equal_device_path": bool(e2e_pg_parity),
-                                "path": "fkd_run_batch with NumPy (pageable) buffers, as flatkd::b200::run_batch "
+                                "path": "same call with NumPy (pageable) buffers, as flatkd::b200::run_batch "
                                         "passes a reference BatchResult's std::vectors"}
     if line.get("issue_roofline"):
         line["issue_roofline"]["frac"] = line["issue_roofline"]["achieved"] / line["issue_roofline"]["peak"]

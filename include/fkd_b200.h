@@ -134,6 +134,25 @@ fkd_status fkd_run_batch(const fkd_tree* tree, const float* queries, int64_t m, 
                          const fkd_batch_options* opt, int32_t* counts, fkd_hit* hits,
                          fkd_query_stats* stats);
 
+/* One host-buffer batch of fkd_run_batches. */
+typedef struct fkd_host_batch {
+    const float* queries;     /* m x dim, host                               */
+    int64_t m;
+    int32_t dim;
+    fkd_batch_options opt;
+    int32_t* counts;          /* [m], host                                   */
+    fkd_hit* hits;            /* [m * stride], host                          */
+    fkd_query_stats* stats;   /* may be NULL                                 */
+    fkd_status status;        /* out: this batch's status                    */
+} fkd_host_batch;
+
+/* Several host-buffer batches in one call.  Batches over the same query
+ * array (same pointer, m and dim) run as one pipeline: the queries are
+ * uploaded, checked and Morton-ordered once per chunk and walked by every
+ * batch of the group; other batches run afterwards.  Each batch keeps its own
+ * results, counters and status; returns the first non-OK status. */
+fkd_status fkd_run_batches(const fkd_tree* tree, fkd_host_batch* batches, int32_t n);
+
 /* Device buffers on the tree's first device, launched on `stream` (a
  * cudaStream_t; NULL = legacy default stream).  The kernels are enqueued on
  * `stream`; the call then synchronises that stream once, because the

@@ -35,13 +35,13 @@ from typing import List, Optional, Sequence
 
 import numpy as np
 
-from ._lib import LIB, LIB_PATH, fkd_batch_options, fkd_device_batch, fkd_query_stats, fkd_timings
+from ._lib import LIB, LIB_PATH, fkd_batch_options, fkd_device_batch, fkd_host_batch, fkd_query_stats, fkd_timings
 
 __all__ = [
     "BatchOptions", "BatchResult", "DataError", "DeviceError", "Engine", "HIT_DTYPE",
     "InvalidArgument", "InvariantError", "KdTree", "QueryKind", "QueryStats", "build_tree",
     "build_level_order", "build_level_order_device", "clustered_points", "fcp", "knn", "random_points", "result_hash", "run_batch",
-    "run_batch_device", "run_batches_device", "write_query_results", "LIB_PATH",
+    "run_batch_device", "run_batches", "run_batches_device", "write_query_results", "LIB_PATH",
 ]
 
 HIT_DTYPE = np.dtype([("node", "<i4"), ("dist2", "<f4")])  # flatkd::Hit, 8 bytes
@@ -296,6 +296,39 @@ def run_batch(tree: KdTree, queries, options: Optional[BatchOptions] = None) -> 
     _check(LIB.fkd_run_batch(tree.handle, q.ctypes.data, m, dim, C.byref(o), counts.ctypes.data,
                              hits.ctypes.data, C.byref(st)))
     return BatchResult(stride, counts, hits, QueryStats.from_c(st) if options.collect_stats else QueryStats())
+
+
+def run_batches(tree: KdTree, batches) -> List[BatchResult]:
+    """Several host-buffer batches in one call (fkd_run_batches): ``batches``
+    is a list of (queries, BatchOptions).  Batches over the same query array
+    (the same object) run as one pipeline — the queries are uploaded, checked
+    and ordered once per chunk and walked by every batch.  Returns one
+    BatchResult per batch; raises on the first failing batch."""
+    n = len(batches)
+    arr = (fkd_host_batch * max(n, 1))()
+    keep, results = [], []
+    converted = {}
+    for i, (queries, opt) in enumerate(batches):
+        opt = opt or BatchOptions()
+        if opt.kind == QueryKind.knn and opt.k < 1:  # batch.cpp:72-73, checked first
+            raise InvalidArgument("knn: k must be >= 1")
+        q = converted.get(id(queries))
+        if q is None:
+            q = converted[id(queries)] = _f32(queries, tree.dim())
+        if q.ndim != 2:
+            raise DataError("queries: expected an (m, dim) array")
+        m, dim = q.shape
+        counts = np.zeros(m, np.int32)
+        hits = np.empty(m * opt.stride, HIT_DTYPE)
+        st = fkd_query_stats()
+        keep.append((q, counts, hits, st))
+        results.append((opt, counts, hits, st))
+        b = arr[i]
+        b.queries, b.m, b.dim, b.opt = q.ctypes.data, m, dim, opt.to_c()
+        b.counts, b.hits, b.stats = counts.ctypes.data, hits.ctypes.data, C.addressof(st)
+    _check(LIB.fkd_run_batches(tree.handle, arr, n))
+    return [BatchResult(opt.stride, c, h, QueryStats.from_c(st) if opt.collect_stats else QueryStats())
+            for opt, c, h, st in results]
 
 
 def _stream_ptr(stream):

@@ -13,7 +13,7 @@ LIB_PATH = os.environ.get("FKD_LIB") or os.path.join(HERE, "libfkd_b200.so")  # 
 # every symbol include/fkd_b200.h declares
 EXPORTS = (
     "fkd_default_options", "fkd_tree_create", "fkd_tree_create_device", "fkd_tree_destroy",
-    "fkd_tree_size", "fkd_tree_dim", "fkd_tree_replicas", "fkd_tree_add_replicas", "fkd_run_batch", "fkd_run_batch_device", "fkd_run_batches_device", "fkd_fcp", "fkd_knn",
+    "fkd_tree_size", "fkd_tree_dim", "fkd_tree_replicas", "fkd_tree_add_replicas", "fkd_run_batch", "fkd_run_batches", "fkd_run_batch_device", "fkd_run_batches_device", "fkd_fcp", "fkd_knn",
     "fkd_build_tree", "fkd_build_tree_device", "fkd_tree_build", "fkd_result_hash", "fkd_random_points", "fkd_clustered_points",
     "fkd_host_alloc", "fkd_host_free", "fkd_last_error", "fkd_version", "fkd_trace_batch",
     "fkd_file_info", "fkd_read_file_device", "fkd_write_file", "fkd_tree_load",
@@ -41,6 +41,11 @@ class fkd_device_batch(C.Structure):
                 ("d_per_query", C.c_void_p), ("timings", C.c_void_p), ("status", C.c_int32)]
 
 
+class fkd_host_batch(C.Structure):
+    _fields_ = [("queries", C.c_void_p), ("m", C.c_int64), ("dim", C.c_int32), ("opt", fkd_batch_options),
+                ("counts", C.c_void_p), ("hits", C.c_void_p), ("stats", C.c_void_p), ("status", C.c_int32)]
+
+
 def _load() -> C.CDLL:
     if not os.path.exists(LIB_PATH):
         raise ImportError(
@@ -64,6 +69,7 @@ def _load() -> C.CDLL:
     lib.fkd_run_batch.argtypes = [vp, vp, i64, i32, vp, vp, vp, vp]
     lib.fkd_run_batch_device.argtypes = [vp, vp, i64, i32, vp, vp, vp, vp, vp, vp, vp]
     lib.fkd_run_batches_device.argtypes = [vp, vp, i32, vp]
+    lib.fkd_run_batches.argtypes = [vp, vp, i32]
     lib.fkd_fcp.argtypes = [vp, vp, i32, C.c_float, vp, vp, vp]
     lib.fkd_knn.argtypes = [vp, vp, i32, i32, C.c_float, vp, vp, vp]
     lib.fkd_build_tree.argtypes = [vp, i64, i32, vp]

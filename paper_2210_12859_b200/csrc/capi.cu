@@ -46,6 +46,9 @@ fkd_status fail(fkd_status s, const std::string& msg) {
     } while (0)
 
 constexpr int64_t kSortChunk = int64_t(1) << 30;  // u32 ids, int item counts in CUB
+constexpr int kSmallWords = 64;   // per-workspace device counters (Workspace::small)
+constexpr int kBatchTotals = 16;  // first per-batch totals word
+constexpr int kMaxGroup = (kSmallWords - kBatchTotals) / 3;  // batches per host pipeline
 
 int walk_bucket_of(int k);
 // The rounds run for register lists of <= 4 slots (fcp, k <= 4) and, in
@@ -126,7 +129,10 @@ struct Workspace {
     int64_t key_cap = 0;
     void* sort_tmp = nullptr;
     size_t sort_tmp_bytes = 0;
-    unsigned long long* small = nullptr;    // [8]: bad, steps, visited, processed, work, ovf count, ovf next
+    // [kSmallWords]: 0 bad, 1-3 steps/visited/processed, 5-6 ovf count/next,
+    // 8 resume count, 10 round count; from kBatchTotals: 3 totals per batch
+    // of a multi-batch host pipeline
+    unsigned long long* small = nullptr;
     uint32_t* ovf = nullptr;                // overflow query ids
     int64_t ovf_cap = 0;
     uint32_t* wave_ids = nullptr;           // [2 * cap] parked-id lists (rounds, resume pass)
@@ -465,8 +471,8 @@ fkd_status acquire_ws(Replica& r, Workspace** out) {
         cudaDeviceGetStreamPriorityRange(&lo, &hi);
         e = cudaStreamCreateWithPriority(&w->tail, cudaStreamNonBlocking, hi);
     }
-    if (e == cudaSuccess) e = cudaMalloc(&w->small, 16 * sizeof(unsigned long long));
-    if (e == cudaSuccess) e = cudaMallocHost(&w->h_small, 16 * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMalloc(&w->small, kSmallWords * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMallocHost(&w->h_small, kSmallWords * sizeof(unsigned long long));
     if (e != cudaSuccess) {
         delete w;
         return fail(FKD_CUDA_ERROR, std::string("workspace: ") + cudaGetErrorString(e));
@@ -543,7 +549,8 @@ fkd_status enqueue(const fkd_tree* t, Replica& r, Workspace* w, const float* d_q
                    fkd_query_stats* d_per_query, bool stats, cudaStream_t st, int* launches,
                    int* walk_launches, const Knobs& tu, cudaEvent_t ev_mid, cudaEvent_t ev_tail = nullptr,
                    int64_t id_offset = 0, cudaStream_t tail_st = nullptr, int budget_div = 1,
-                   const SharedOrder* share = nullptr, cudaEvent_t ev_sorted = nullptr) {
+                   const SharedOrder* share = nullptr, cudaEvent_t ev_sorted = nullptr,
+                   unsigned long long* totals = nullptr) {
     const int k = o->kind == FKD_KNN ? o->k : 1;
     if (t->n == 0) {  // every query returns empty; queries are not read (batch.cpp:75)
         *launches += fill_empty(d_counts, d_hits, m, k, st);
@@ -598,7 +605,7 @@ fkd_status enqueue(const fkd_tree* t, Replica& r, Workspace* w, const float* d_q
         a.recursive_stats = o->engine == FKD_ENGINE_RECURSIVE;
         a.counts = d_counts + base;
         a.hits = d_hits + base * k;
-        a.totals = w->small + 1;
+        a.totals = totals ? totals : w->small + 1;
         a.per_query = d_per_query ? d_per_query + base : nullptr;
         a.bad = w->small;
         a.id_base = id_offset + base;
@@ -1299,31 +1306,33 @@ fkd_status fkd_run_batches_device(const fkd_tree* t, fkd_device_batch* batches, 
 
 }  // extern "C"
 
-// ---- host-buffer path (fkd_run_batch) --------------------------------------
+// ---- host-buffer path (fkd_run_batch, fkd_run_batches) ---------------------
 //
 // The batch is sharded over the tree's devices in contiguous blocks (the
 // reference's OpenMP loop over queries, batch.cpp:93-103, lifted to devices);
 // each device's shard runs as its own pipeline, enqueued by its own host
 // thread.  Per device, the shard is cut into a graduated chunk schedule —
-// small first chunks (the first H2D + walk overlap nothing), shard/8 middle
-// chunks, small last chunks (the last D2H overlaps nothing) — walked on
-// `streams` slot streams so the H2D engine, the SMs and the D2H engine stay
-// busy at once:
-//   copy-in stream : H2D chunk c                       -> ev_in[c]
-//   slot stream    : wait ev_in[c]; order + walk       -> ev_walk[c]
-//   copy-out stream: wait ev_walk[c]; D2H counts, hits -> ev_out[c]
-// Device staging is "full" when the shard's queries and results fit in a
-// quarter of the free memory (all H2Ds are then issued up front, so the
-// copy-in finishes before it shares PCIe with the copy-out); otherwise each
-// slot holds its largest chunk and chunk c reuses slot c mod R after the
-// slot's previous walk / D2H.
+// small first chunks (the first H2D + walk overlap nothing), shard/div middle
+// chunks, small last chunks (the last D2H overlaps nothing) — and every chunk
+// is one job per batch of the group (the batches of one fkd_run_batches call
+// over the same query array: the chunk's queries are uploaded, checked and
+// Morton-ordered once and walked by every batch).  Jobs run on `streams`
+// slot streams, so the H2D engine, the SMs and the D2H engine stay busy:
+//   copy-in stream : H2D chunk c                          -> ev_in[c]
+//   slot stream    : wait ev_in[c]; order + walk (job j)  -> ev_walk[j]
+//   copy-out stream: wait ev_walk[j]; D2H counts, hits    -> ev_out[j]
+// Device staging is "full" when the shard's queries and every batch's results
+// fit in a quarter of the free memory (all H2Ds are then issued up front, so
+// the copy-in finishes before it shares PCIe with the copy-out); otherwise a
+// chunk's queries live in its first job's slot and each job's results in its
+// own slot, reused R jobs later once the previous users are done.
 //
 // Pageable caller buffers (std::vector / NumPy: what a reference caller
 // holds) are staged through bounded rings of pinned host slots: a query
 // chunk is copied into its ring slot by the host copy pool just before its
 // H2D (the copy also runs require_finite, batch.cpp:79), and a drain thread
-// enqueues each chunk's D2H into a result ring slot and copies the slot out
-// to the caller once the D2H has landed, R chunks behind.  Results reach the
+// enqueues each job's D2H into a result ring slot and copies the slot out
+// to the caller once the D2H has landed, R jobs behind.  Results reach the
 // caller's buffers only after every query of the batch passed the host check,
 // so a rejected batch leaves pageable outputs untouched, as the reference
 // throws before its BatchResult exists (batch.cpp:79 before :82-86).
@@ -1332,23 +1341,34 @@ fkd_status fkd_run_batches_device(const fkd_tree* t, fkd_device_batch* batches, 
 namespace fkd {
 namespace {
 
+struct GroupBatch {  // one batch of a host group (all share the query array)
+    const fkd_batch_options* o = nullptr;
+    float cap2 = 0.0f;
+    int k = 1;
+    int32_t* counts = nullptr;
+    fkd_hit* hits = nullptr;
+    bool want_stats = false;
+    fkd_query_stats* stats = nullptr;
+};
 
 struct PipeJob {
-    int64_t base, count, off;  // global query offset, size, offset in the device's shard
-    int ws;                    // slot (workspace) index
+    int64_t base, count, off;  // the chunk: global query offset, size, offset in the device's shard
+    int chunk, b, ws;          // chunk index, batch index, slot (workspace) index
 };
 
 struct DevicePipe {
     int di = 0;
     Replica* rep = nullptr;
     std::vector<Workspace*> wss;
-    std::vector<PipeJob> jobs;
+    std::vector<PipeJob> jobs;  // chunk-major, batch-minor
+    int nchunks = 0;
     bool full = false;
     bool pg_q = false, pg_out = false;
     HostStage qst{}, rst{};
-    int64_t max_chunk = 0;
+    int64_t max_chunk = 0, qring = 1, rring = 1;
     size_t r_slot_bytes = 0;
-    std::vector<cudaEvent_t> ev_in, ev_walk, ev_out;
+    std::vector<cudaEvent_t> ev_in;                    // per chunk
+    std::vector<cudaEvent_t> ev_sorted, ev_walk, ev_out;  // per job
     // enqueue thread -> drain thread hand-off
     std::mutex mu;
     std::condition_variable cv;
@@ -1414,21 +1434,17 @@ std::vector<int64_t> chunk_schedule(const Knobs& kn, int64_t total, int64_t full
     return sizes;
 }
 
-}  // namespace
-}  // namespace fkd
-
-fkd_status fkd_run_batch(const fkd_tree* t, const float* queries, int64_t m, int32_t dim,
-                         const fkd_batch_options* o, int32_t* counts, fkd_hit* hits,
-                         fkd_query_stats* stats) {
-    float cap2 = 0.0f;
-    fkd_status s = validate(t, m, dim, o, &cap2);
-    if (s != FKD_OK) return s;
-    if (stats) *stats = fkd_query_stats{0, 0, 0};
-    if (m == 0) return FKD_OK;
-    if (t->reps.empty()) return fail(FKD_NO_DEVICE, "tree has no device replica");
-    const Knobs kn = read_knobs();
-    const int k = o->kind == FKD_KNN ? o->k : 1;
-    const bool want_stats = o->collect_stats != 0;
+// The chunked pipeline over one query array and the batches of its group
+// (validated by the caller; m > 0, 1 <= group size <= kMaxGroup).
+fkd_status run_host_group(const fkd_tree* t, const float* queries, int64_t m, int32_t dim,
+                          std::vector<GroupBatch>& batches, const Knobs& kn) {
+    const int B = int(batches.size());
+    int kmax = 1;
+    double out_bytes_per_query = 0.0;
+    for (const GroupBatch& g : batches) {
+        kmax = std::max(kmax, g.k);
+        out_bytes_per_query += 4.0 + 8.0 * g.k;
+    }
     const bool check = t->n > 0;  // require_finite only with a non-empty tree (batch.cpp:75)
     const int ndev = int(t->reps.size());
     const int64_t per_dev = (m + ndev - 1) / ndev;
@@ -1436,18 +1452,20 @@ fkd_status fkd_run_batch(const fkd_tree* t, const float* queries, int64_t m, int
     // 15.6 ms vs 16.3 at 4); 4 for one-slot results, whose call is bound by
     // the chunk walks (C3 fcp pageable 9.4 -> 7.4 ms, pinned 4.7 -> 4.6;
     // tools/e2e_ab.py, profiles/r02/r02h_e2e_ab.log)
-    const int64_t div = kn.chunk_div > 0 ? kn.chunk_div : (k == 1 ? 4 : 8);
+    const int64_t div = kn.chunk_div > 0 ? kn.chunk_div : (kmax == 1 ? 4 : 8);
     const int64_t full_chunk = kn.chunk > 0 ? kn.chunk
                                             : std::min<int64_t>(int64_t(4) << 20,
                                                                 std::max<int64_t>(int64_t(256) << 10,
                                                                                   (per_dev + div - 1) / div));
-    const bool want_pg_q = kn.pageable_staging && is_pageable(queries);
-    const bool want_pg_out = kn.pageable_staging && (is_pageable(counts) || is_pageable(hits));
+    bool want_pg_q = kn.pageable_staging && is_pageable(queries);
+    bool want_pg_out = false;
+    for (const GroupBatch& g : batches)
+        want_pg_out |= kn.pageable_staging && (is_pageable(g.counts) || is_pageable(g.hits));
 
     std::vector<std::unique_ptr<DevicePipe>> pipes;
     PipeShared sh;
     fkd_status err = FKD_OK;
-    // ---- plan: shards, chunks, slots, device staging, host rings, events
+    // ---- plan: shards, chunks, jobs, slots, device staging, host rings, events
     for (int di = 0; di < ndev && err == FKD_OK; ++di) {
         const int64_t lo = std::min<int64_t>(m, di * per_dev), hi = std::min<int64_t>(m, lo + per_dev);
         if (hi <= lo) continue;
@@ -1456,7 +1474,11 @@ fkd_status fkd_run_batch(const fkd_tree* t, const float* queries, int64_t m, int
         P->rep = t->reps[di];
         DeviceGuard g(P->rep->device);
         const std::vector<int64_t> sizes = chunk_schedule(kn, hi - lo, full_chunk);
-        const int nws = int(std::min<size_t>(sizes.size(), size_t(kn.streams)));
+        P->nchunks = int(sizes.size());
+        const size_t njobs = sizes.size() * size_t(B);
+        // at least one slot per batch: in full staging batch b keeps its
+        // results in slot b's buffers
+        const int nws = int(std::max<size_t>(size_t(B), std::min<size_t>(njobs, size_t(kn.streams))));
         for (int j = 0; j < nws && err == FKD_OK; ++j) {
             Workspace* w = nullptr;
             err = acquire_ws(*P->rep, &w);
@@ -1469,54 +1491,76 @@ fkd_status fkd_run_batch(const fkd_tree* t, const float* queries, int64_t m, int
         // the workspace that already holds the largest staging serves as slot 0
         std::stable_sort(P->wss.begin(), P->wss.end(),
                          [](const Workspace* x, const Workspace* y) { return x->h_cap > y->h_cap; });
-        int64_t b = lo;
+        int64_t base = lo;
         for (size_t c = 0; c < sizes.size(); ++c) {
-            P->jobs.push_back(PipeJob{b, sizes[c], b - lo, int(c % P->wss.size())});
+            for (int b = 0; b < B; ++b) {
+                const size_t j = P->jobs.size();
+                P->jobs.push_back(PipeJob{base, sizes[c], base - lo, int(c), b, int(j % P->wss.size())});
+            }
             P->max_chunk = std::max(P->max_chunk, sizes[c]);
-            b += sizes[c];
+            base += sizes[c];
         }
         const int64_t shard = hi - lo;
         Workspace* w0 = P->wss[0];
-        const int64_t have = std::min({w0->q_cap / std::max(1, dim), w0->c_cap, w0->h_cap / k});
-        bool fits = have >= shard;
+        bool fits = w0->q_cap >= shard * dim;
+        for (int b = 0; b < B && fits; ++b)
+            fits = P->wss[size_t(b)]->c_cap >= shard && P->wss[size_t(b)]->h_cap >= shard * batches[size_t(b)].k;
         if (!fits && kn.full_staging) {
             size_t free_b = 0, total_b = 0;
             cudaMemGetInfo(&free_b, &total_b);
-            fits = double(shard) * (double(dim) * 4 + 4 + 8.0 * k) <= 0.25 * double(free_b);
+            fits = double(shard) * (double(dim) * 4 + out_bytes_per_query) <= 0.25 * double(free_b);
         }
         P->full = kn.full_staging && fits;
         for (size_t wi = 0; wi < P->wss.size() && err == FKD_OK; ++wi) {
             Workspace* w = P->wss[wi];
-            int64_t big = 0;
-            for (const PipeJob& j : P->jobs)
-                if (j.ws == int(wi)) big = std::max(big, j.count);
-            if (P->full) big = wi == 0 ? shard : 0;
-            cudaError_t e = grow(w->q, w->q_cap, big * dim);
-            if (e == cudaSuccess) e = grow(w->counts, w->c_cap, big);
-            if (e == cudaSuccess) e = grow(w->hits, w->h_cap, big * k);
+            int64_t q_need = 0, c_need = 0, h_need = 0;
+            if (P->full) {
+                if (wi == 0) q_need = shard * dim;
+                if (int(wi) < B) {
+                    c_need = shard;
+                    h_need = shard * batches[wi].k;
+                }
+            } else {
+                for (const PipeJob& jb : P->jobs)
+                    if (jb.ws == int(wi)) {
+                        if (jb.b == 0) q_need = std::max(q_need, jb.count * dim);  // the chunk's query buffer
+                        c_need = std::max(c_need, jb.count);
+                        h_need = std::max(h_need, jb.count * batches[size_t(jb.b)].k);
+                    }
+            }
+            cudaError_t e = grow(w->q, w->q_cap, q_need);
+            if (e == cudaSuccess) e = grow(w->counts, w->c_cap, c_need);
+            if (e == cudaSuccess) e = grow(w->hits, w->h_cap, h_need);
             if (e != cudaSuccess) err = fail(FKD_CUDA_ERROR, std::string("staging: ") + cudaGetErrorString(e));
         }
         // pinned host rings for pageable caller buffers (fall back to direct
         // pageable copies when pinned memory is not available)
-        const int64_t ring = std::min<int64_t>(kn.host_ring, int64_t(P->jobs.size()));
+        P->qring = std::min<int64_t>(kn.host_ring, P->nchunks);
+        P->rring = std::min<int64_t>(int64_t(kn.host_ring) * B, int64_t(P->jobs.size()));
         if (err == FKD_OK && want_pg_q) {
-            P->pg_q = acquire_stage(size_t(ring * P->max_chunk) * dim * sizeof(float), &P->qst) == cudaSuccess;
+            P->pg_q = acquire_stage(size_t(P->qring * P->max_chunk) * dim * sizeof(float), &P->qst) == cudaSuccess;
             if (!P->pg_q) cudaGetLastError();
         }
         if (err == FKD_OK && want_pg_out) {
-            P->r_slot_bytes = (size_t(P->max_chunk) * (sizeof(int32_t) + size_t(k) * sizeof(fkd_hit)) + 255) & ~size_t(255);
-            P->pg_out = acquire_stage(size_t(ring) * P->r_slot_bytes, &P->rst) == cudaSuccess;
+            P->r_slot_bytes = (size_t(P->max_chunk) * (sizeof(int32_t) + size_t(kmax) * sizeof(fkd_hit)) + 255) &
+                              ~size_t(255);
+            P->pg_out = acquire_stage(size_t(P->rring) * P->r_slot_bytes, &P->rst) == cudaSuccess;
             if (!P->pg_out) cudaGetLastError();
         }
-        for (auto* v : {&P->ev_in, &P->ev_walk, &P->ev_out}) {
-            v->assign(P->jobs.size(), nullptr);
+        P->ev_in.assign(size_t(P->nchunks), nullptr);
+        for (auto* v : {&P->ev_sorted, &P->ev_walk, &P->ev_out}) v->assign(P->jobs.size(), nullptr);
+        for (auto* v : {&P->ev_in, &P->ev_sorted, &P->ev_walk, &P->ev_out})
             for (auto& e : *v)
                 if (err == FKD_OK && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
                     err = fail(FKD_CUDA_ERROR, "event create failed");
-        }
         for (Workspace* w : P->wss) {
             cudaError_t e = reset_small(w, w->stream);
             if (e != cudaSuccess && err == FKD_OK) err = fail(FKD_CUDA_ERROR, std::string("reset: ") + cudaGetErrorString(e));
+        }
+        if (err == FKD_OK) {  // per-batch totals in slot 0's counter block
+            cudaError_t e = cudaMemsetAsync(w0->small + kBatchTotals, 0, size_t(3 * B) * sizeof(unsigned long long),
+                                            w0->stream);
+            if (e != cudaSuccess) err = fail(FKD_CUDA_ERROR, std::string("reset: ") + cudaGetErrorString(e));
         }
         pipes.push_back(std::move(P));
     }
@@ -1540,70 +1584,113 @@ fkd_status fkd_run_batch(const fkd_tree* t, const float* queries, int64_t m, int
     sh.checks_left = int(pipes.size());
 
     // ---- per-device enqueue (and drain) threads
+    auto job_results = [&](DevicePipe& P, const PipeJob& jb, int32_t** dc, fkd_hit** dh) {
+        if (P.full) {
+            Workspace* rb = P.wss[size_t(jb.b)];
+            *dc = rb->counts + jb.off;
+            *dh = rb->hits + jb.off * batches[size_t(jb.b)].k;
+        } else {
+            *dc = P.wss[size_t(jb.ws)]->counts;
+            *dh = P.wss[size_t(jb.ws)]->hits;
+        }
+    };
     auto enqueue_pipe = [&](DevicePipe& P) {
         DeviceGuard g(P.rep->device);
         Workspace* io = P.wss[0];
-        const int64_t ring = std::min<int64_t>(kn.host_ring, int64_t(P.jobs.size()));
-        std::vector<int64_t> last_on_ws(P.wss.size(), -1);
-        for (size_t c = 0; c < P.jobs.size() && !sh.stop; ++c) {
-            const PipeJob& j = P.jobs[c];
-            Workspace* w = P.wss[size_t(j.ws)];
-            const int64_t prev = last_on_ws[size_t(j.ws)];
-            last_on_ws[size_t(j.ws)] = int64_t(c);
-            const bool dring = !P.full;
-            float* dq = dring ? w->q : io->q + j.off * dim;
-            int32_t* dc = dring ? w->counts : io->counts + j.off;
-            fkd_hit* dh = dring ? w->hits : io->hits + j.off * k;
-            const float* src = queries + j.base * dim;
-            auto cuda = [&](cudaError_t e, const char* what) {
-                if (e != cudaSuccess) sh.error(FKD_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
-                return e == cudaSuccess;
-            };
+        std::vector<int64_t> last_job_on_ws(P.wss.size(), -1);
+        // jobs that still read a slot's query buffer / Morton order
+        std::vector<std::vector<size_t>> q_readers(P.wss.size()), order_readers(P.wss.size());
+        auto cuda = [&](cudaError_t e, const char* what) {
+            if (e != cudaSuccess) sh.error(FKD_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+            return e == cudaSuccess;
+        };
+        bool stop = false;
+        for (int c = 0; c < P.nchunks && !stop && !sh.stop; ++c) {
+            const size_t j0 = size_t(c) * size_t(B);
+            const PipeJob& first = P.jobs[j0];
+            Workspace* qw = P.wss[size_t(first.ws)];  // ring staging: the chunk's query buffer
+            float* dq = P.full ? io->q + first.off * dim : qw->q;
+            const float* src = queries + first.base * dim;
             if (P.pg_q) {
-                const int64_t slot = int64_t(c) % ring;
-                if (int64_t(c) >= ring && !cuda(cudaEventSynchronize(P.ev_in[c - size_t(ring)]), "staging")) break;
+                const int64_t slot = c % P.qring;
+                if (c >= P.qring && !cuda(cudaEventSynchronize(P.ev_in[size_t(c - P.qring)]), "staging")) break;
                 float* stq = reinterpret_cast<float*>(P.qst.p) + slot * P.max_chunk * dim;
-                const int64_t f = par_copy_check(stq, src, j.count * dim);
+                const int64_t f = par_copy_check(stq, src, first.count * dim);
                 if (check && f >= 0) {  // this and later chunks are not walked
-                    sh.bad((unsigned long long)(j.base + f / dim));
+                    sh.bad((unsigned long long)(first.base + f / dim));
                     break;
                 }
                 src = stq;
             }
-            if (dring && prev >= 0 && !cuda(cudaStreamWaitEvent(io->cin, P.ev_walk[size_t(prev)], 0), "wait")) break;
-            if (!cuda(cudaMemcpyAsync(dq, src, size_t(j.count) * dim * sizeof(float), cudaMemcpyHostToDevice, io->cin), "H2D") ||
-                !cuda(cudaEventRecord(P.ev_in[c], io->cin), "event") ||
-                !cuda(cudaStreamWaitEvent(w->stream, P.ev_in[c], 0), "wait"))
+            if (!P.full)  // the query buffer's previous readers are done
+                for (size_t r : q_readers[size_t(first.ws)])
+                    if (!cuda(cudaStreamWaitEvent(io->cin, P.ev_walk[r], 0), "wait")) stop = true;
+            if (stop ||
+                !cuda(cudaMemcpyAsync(dq, src, size_t(first.count) * dim * sizeof(float), cudaMemcpyHostToDevice,
+                                      io->cin), "H2D") ||
+                !cuda(cudaEventRecord(P.ev_in[size_t(c)], io->cin), "event"))
                 break;
-            if (dring && prev >= 0) {  // the slot's results buffer: its previous D2H must be enqueued and done
-                if (P.pg_out) {
-                    std::unique_lock<std::mutex> lk(P.mu);
-                    P.cv.wait(lk, [&] { return P.d2h_enqueued > size_t(prev) || sh.stop; });
-                    if (sh.stop) break;
+            q_readers[size_t(first.ws)].clear();
+            SharedOrder share{};
+            for (int b = 0; b < B && !stop; ++b) {
+                const size_t j = j0 + size_t(b);
+                const PipeJob& jb = P.jobs[j];
+                const GroupBatch& gb = batches[size_t(b)];
+                Workspace* w = P.wss[size_t(jb.ws)];
+                const int64_t prev = last_job_on_ws[size_t(jb.ws)];
+                last_job_on_ws[size_t(jb.ws)] = int64_t(j);
+                int32_t* dc = nullptr;
+                fkd_hit* dh = nullptr;
+                job_results(P, jb, &dc, &dh);
+                if (!cuda(cudaStreamWaitEvent(w->stream, P.ev_in[size_t(c)], 0), "wait")) break;
+                // this slot's Morton order may still be read by another batch's walk
+                for (size_t r : order_readers[size_t(jb.ws)])
+                    if (!cuda(cudaStreamWaitEvent(w->stream, P.ev_walk[r], 0), "wait")) stop = true;
+                order_readers[size_t(jb.ws)].clear();
+                if (!P.full && prev >= 0) {  // the slot's results buffer: its previous D2H must be done
+                    if (P.pg_out) {
+                        std::unique_lock<std::mutex> lk(P.mu);
+                        P.cv.wait(lk, [&] { return P.d2h_enqueued > size_t(prev) || sh.stop; });
+                        if (sh.stop) stop = true;
+                    }
+                    if (!stop && !cuda(cudaStreamWaitEvent(w->stream, P.ev_out[size_t(prev)], 0), "wait")) stop = true;
                 }
-                if (!cuda(cudaStreamWaitEvent(w->stream, P.ev_out[size_t(prev)], 0), "wait")) break;
-            }
-            int launches = 0, wl = 0;
-            const fkd_status e = enqueue(t, *P.rep, w, dq, j.count, o, cap2, dc, dh, nullptr, want_stats, w->stream,
-                                         &launches, &wl, kn, nullptr, nullptr, j.base, w->tail,
-                                         c == 0 ? kn.first_budget_div : 1);
-            if (e != FKD_OK) {
-                sh.error(e, g_err);
-                break;
-            }
-            if (!cuda(cudaEventRecord(P.ev_walk[c], w->stream), "event")) break;
-            if (!P.pg_out) {
-                if (!cuda(cudaStreamWaitEvent(io->cout, P.ev_walk[c], 0), "wait") ||
-                    !cuda(cudaMemcpyAsync(counts + j.base, dc, size_t(j.count) * sizeof(int32_t),
-                                          cudaMemcpyDeviceToHost, io->cout), "D2H") ||
-                    !cuda(cudaMemcpyAsync(hits + j.base * k, dh, size_t(j.count) * k * sizeof(fkd_hit),
-                                          cudaMemcpyDeviceToHost, io->cout), "D2H") ||
-                    !cuda(cudaEventRecord(P.ev_out[c], io->cout), "event"))
+                if (stop) break;
+                int launches = 0, wl = 0;
+                const bool sharing = b > 0 && share.order != nullptr && use_morton(t, gb.o, jb.count);
+                const fkd_status e =
+                    enqueue(t, *P.rep, w, dq, jb.count, gb.o, gb.cap2, dc, dh, nullptr, gb.want_stats, w->stream,
+                            &launches, &wl, kn, nullptr, nullptr, jb.base, w->tail, c == 0 ? kn.first_budget_div : 1,
+                            sharing ? &share : nullptr, (b == 0 && B > 1) ? P.ev_sorted[j] : nullptr,
+                            io->small + kBatchTotals + 3 * b);
+                if (e != FKD_OK) {
+                    sh.error(e, g_err);
+                    stop = true;
                     break;
-            } else {
-                std::lock_guard<std::mutex> lk(P.mu);
-                P.enqueued = c + 1;
-                P.cv.notify_all();
+                }
+                if (b == 0 && B > 1 && use_morton(t, gb.o, jb.count) && jb.count <= kSortChunk)
+                    share = SharedOrder{w->ids + w->key_cap / 2, w->small, P.ev_sorted[j]};
+                if (!cuda(cudaEventRecord(P.ev_walk[j], w->stream), "event")) {
+                    stop = true;
+                    break;
+                }
+                q_readers[size_t(first.ws)].push_back(j);
+                if (sharing) order_readers[size_t(first.ws)].push_back(j);
+                if (!P.pg_out) {
+                    if (!cuda(cudaStreamWaitEvent(io->cout, P.ev_walk[j], 0), "wait") ||
+                        !cuda(cudaMemcpyAsync(gb.counts + jb.base, dc, size_t(jb.count) * sizeof(int32_t),
+                                              cudaMemcpyDeviceToHost, io->cout), "D2H") ||
+                        !cuda(cudaMemcpyAsync(gb.hits + jb.base * gb.k, dh, size_t(jb.count) * gb.k * sizeof(fkd_hit),
+                                              cudaMemcpyDeviceToHost, io->cout), "D2H") ||
+                        !cuda(cudaEventRecord(P.ev_out[j], io->cout), "event")) {
+                        stop = true;
+                        break;
+                    }
+                } else {
+                    std::lock_guard<std::mutex> lk(P.mu);
+                    P.enqueued = j + 1;
+                    P.cv.notify_all();
+                }
             }
         }
         {
@@ -1616,11 +1703,12 @@ fkd_status fkd_run_batch(const fkd_tree* t, const float* queries, int64_t m, int
     auto drain_pipe = [&](DevicePipe& P) {
         DeviceGuard g(P.rep->device);
         Workspace* io = P.wss[0];
-        const size_t ring = size_t(std::min<int64_t>(kn.host_ring, int64_t(P.jobs.size())));
+        const size_t ring = size_t(P.rring);
         bool gate = false, ok = false;
-        auto copy_out = [&](size_t c) {
-            const PipeJob& j = P.jobs[c];
-            if (cudaEventSynchronize(P.ev_out[c]) != cudaSuccess) {
+        auto copy_out = [&](size_t j) {
+            const PipeJob& jb = P.jobs[j];
+            const GroupBatch& gb = batches[size_t(jb.b)];
+            if (cudaEventSynchronize(P.ev_out[j]) != cudaSuccess) {
                 sh.error(FKD_CUDA_ERROR, "D2H failed");
                 return;
             }
@@ -1629,44 +1717,44 @@ fkd_status fkd_run_batch(const fkd_tree* t, const float* queries, int64_t m, int
                 gate = true;
             }
             if (!ok || sh.stop) return;
-            const char* slot = P.rst.p + (c % ring) * P.r_slot_bytes;
-            par_copy(counts + j.base, slot, size_t(j.count) * sizeof(int32_t));
-            par_copy(hits + j.base * k, slot + size_t(P.max_chunk) * sizeof(int32_t),
-                     size_t(j.count) * k * sizeof(fkd_hit));
+            const char* slot = P.rst.p + (j % ring) * P.r_slot_bytes;
+            par_copy(gb.counts + jb.base, slot, size_t(jb.count) * sizeof(int32_t));
+            par_copy(gb.hits + jb.base * gb.k, slot + size_t(P.max_chunk) * sizeof(int32_t),
+                     size_t(jb.count) * gb.k * sizeof(fkd_hit));
         };
-        size_t c = 0;
-        for (;; ++c) {
+        size_t j = 0;
+        for (;; ++j) {
             {
                 std::unique_lock<std::mutex> lk(P.mu);
-                P.cv.wait(lk, [&] { return P.enqueued > c || P.enq_done; });
-                if (P.enqueued <= c) break;
+                P.cv.wait(lk, [&] { return P.enqueued > j || P.enq_done; });
+                if (P.enqueued <= j) break;
             }
-            if (c >= ring) copy_out(c - ring);
-            const PipeJob& j = P.jobs[c];
-            Workspace* w = P.wss[size_t(j.ws)];
-            const int64_t off = P.full ? j.off : 0;
-            const int32_t* dc = P.full ? io->counts + off : w->counts;
-            const fkd_hit* dh = P.full ? io->hits + off * k : w->hits;
-            char* slot = P.rst.p + (c % ring) * P.r_slot_bytes;
-            bool good = cudaStreamWaitEvent(io->cout, P.ev_walk[c], 0) == cudaSuccess &&
-                        cudaMemcpyAsync(slot, dc, size_t(j.count) * sizeof(int32_t), cudaMemcpyDeviceToHost,
-                                        io->cout) == cudaSuccess &&
-                        cudaMemcpyAsync(slot + size_t(P.max_chunk) * sizeof(int32_t), dh,
-                                        size_t(j.count) * k * sizeof(fkd_hit), cudaMemcpyDeviceToHost,
-                                        io->cout) == cudaSuccess &&
-                        cudaEventRecord(P.ev_out[c], io->cout) == cudaSuccess;
+            if (j >= ring) copy_out(j - ring);
+            const PipeJob& jb = P.jobs[j];
+            const GroupBatch& gb = batches[size_t(jb.b)];
+            int32_t* dc = nullptr;
+            fkd_hit* dh = nullptr;
+            job_results(P, jb, &dc, &dh);
+            char* slot = P.rst.p + (j % ring) * P.r_slot_bytes;
+            const bool good = cudaStreamWaitEvent(io->cout, P.ev_walk[j], 0) == cudaSuccess &&
+                              cudaMemcpyAsync(slot, dc, size_t(jb.count) * sizeof(int32_t), cudaMemcpyDeviceToHost,
+                                              io->cout) == cudaSuccess &&
+                              cudaMemcpyAsync(slot + size_t(P.max_chunk) * sizeof(int32_t), dh,
+                                              size_t(jb.count) * gb.k * sizeof(fkd_hit), cudaMemcpyDeviceToHost,
+                                              io->cout) == cudaSuccess &&
+                              cudaEventRecord(P.ev_out[j], io->cout) == cudaSuccess;
             {
                 std::lock_guard<std::mutex> lk(P.mu);
-                P.d2h_enqueued = c + 1;
+                P.d2h_enqueued = j + 1;
                 P.cv.notify_all();
             }
             if (!good) {
                 sh.error(FKD_CUDA_ERROR, "D2H enqueue failed");
-                ++c;
+                ++j;
                 break;
             }
         }
-        for (size_t cc = c > ring ? c - ring : 0; cc < c; ++cc) copy_out(cc);
+        for (size_t jj = j > ring ? j - ring : 0; jj < j; ++jj) copy_out(jj);
     };
     if (err == FKD_OK) {
         std::vector<std::thread> threads;
@@ -1680,11 +1768,12 @@ fkd_status fkd_run_batch(const fkd_tree* t, const float* queries, int64_t m, int
         if (sh.err != FKD_OK) err = fail(sh.err, sh.msg);
     }
     // ---- drain every stream, read the device flags and totals, release
-    unsigned long long bad = kNoBad, tot[3] = {0, 0, 0};
+    unsigned long long bad = kNoBad;
+    std::vector<unsigned long long> tot(size_t(3 * B), 0ull);
     for (auto& P : pipes) {
         DeviceGuard g(P->rep->device);
         for (Workspace* w : P->wss) {
-            cudaError_t e = cudaMemcpyAsync(w->h_small, w->small, 8 * sizeof(unsigned long long),
+            cudaError_t e = cudaMemcpyAsync(w->h_small, w->small, kSmallWords * sizeof(unsigned long long),
                                             cudaMemcpyDeviceToHost, w->stream);
             if (e != cudaSuccess && err == FKD_OK) err = fail(FKD_CUDA_ERROR, std::string("readback: ") + cudaGetErrorString(e));
         }
@@ -1695,10 +1784,12 @@ fkd_status fkd_run_batch(const fkd_tree* t, const float* queries, int64_t m, int
         for (Workspace* w : P->wss) {
             cudaError_t e = cudaStreamSynchronize(w->stream);
             if (e != cudaSuccess && err == FKD_OK) err = fail(FKD_CUDA_ERROR, std::string("stream: ") + cudaGetErrorString(e));
-            if (err == FKD_OK) finish_small(w, 0, &bad, tot);
-            release_ws(*P->rep, w);
+            if (err == FKD_OK && w->h_small[0] != kNoBad) bad = std::min(bad, (unsigned long long)w->h_small[0]);
         }
-        for (auto* v : {&P->ev_in, &P->ev_walk, &P->ev_out})
+        if (err == FKD_OK)
+            for (int i = 0; i < 3 * B; ++i) tot[size_t(i)] += P->wss[0]->h_small[kBatchTotals + i];
+        for (Workspace* w : P->wss) release_ws(*P->rep, w);
+        for (auto* v : {&P->ev_in, &P->ev_sorted, &P->ev_walk, &P->ev_out})
             for (auto& e : *v)
                 if (e) cudaEventDestroy(e);
         release_stage(P->qst);  // every stream that used them is drained
@@ -1708,7 +1799,99 @@ fkd_status fkd_run_batch(const fkd_tree* t, const float* queries, int64_t m, int
     bad = std::min(bad, sh.host_bad);
     if (bad != kNoBad)
         return fail(FKD_DATA_ERROR, "queries: non-finite coordinate in point " + std::to_string(bad));
-    if (stats) *stats = fkd_query_stats{int64_t(tot[0]), int64_t(tot[1]), int64_t(tot[2])};
+    for (int b = 0; b < B; ++b)
+        if (batches[size_t(b)].stats)
+            *batches[size_t(b)].stats = fkd_query_stats{int64_t(tot[size_t(3 * b)]), int64_t(tot[size_t(3 * b + 1)]),
+                                                        int64_t(tot[size_t(3 * b + 2)])};
+    return FKD_OK;
+}
+
+}  // namespace
+}  // namespace fkd
+
+fkd_status fkd_run_batch(const fkd_tree* t, const float* queries, int64_t m, int32_t dim,
+                         const fkd_batch_options* o, int32_t* counts, fkd_hit* hits,
+                         fkd_query_stats* stats) {
+    float cap2 = 0.0f;
+    fkd_status s = validate(t, m, dim, o, &cap2);
+    if (s != FKD_OK) return s;
+    if (stats) *stats = fkd_query_stats{0, 0, 0};
+    if (m == 0) return FKD_OK;
+    if (t->reps.empty()) return fail(FKD_NO_DEVICE, "tree has no device replica");
+    std::vector<GroupBatch> group(1);
+    group[0].o = o;
+    group[0].cap2 = cap2;
+    group[0].k = o->kind == FKD_KNN ? o->k : 1;
+    group[0].counts = counts;
+    group[0].hits = hits;
+    group[0].want_stats = o->collect_stats != 0;
+    group[0].stats = stats;
+    return run_host_group(t, queries, m, dim, group, read_knobs());
+}
+
+// Several host-buffer batches in one call.  Batches over the same query
+// array (same pointer, m, dim) form a group that runs as ONE pipeline: the
+// queries cross PCIe, are checked and Morton-ordered once per chunk, and
+// every batch of the group walks each chunk, so the copy engines stream the
+// group's results back to back (C3 fcp + kNN8: one upload of 120 MB instead
+// of two, and the fcp walks fill the D2H-bound kNN8 pipeline).  Groups run
+// one after another.  Each batch keeps its own results, counters and status.
+fkd_status fkd_run_batches(const fkd_tree* t, fkd_host_batch* batches, int32_t n) {
+    if (n < 0 || (n > 0 && !batches)) return fail(FKD_INVALID_ARGUMENT, "bad batch list");
+    fkd_status first = FKD_OK;
+    std::string first_msg;
+    auto note = [&](fkd_host_batch* b, fkd_status s) {
+        b->status = s;
+        if (s != FKD_OK && first == FKD_OK) {
+            first = s;
+            first_msg = g_err;
+        }
+    };
+    std::vector<char> done(size_t(n), 0);
+    std::vector<float> cap2(size_t(n), 0.0f);
+    for (int32_t i = 0; i < n; ++i) {
+        fkd_host_batch* b = &batches[i];
+        b->status = FKD_OK;
+        if (b->stats) *b->stats = fkd_query_stats{0, 0, 0};
+        fkd_status s = validate(t, b->m, b->dim, &b->opt, &cap2[size_t(i)]);
+        if (s == FKD_OK && b->m > 0 && t->reps.empty()) s = fail(FKD_NO_DEVICE, "tree has no device replica");
+        if (s != FKD_OK || b->m == 0) {
+            note(b, s);
+            done[size_t(i)] = 1;
+        }
+    }
+    const Knobs kn = read_knobs();
+    for (int32_t i = 0; i < n; ++i) {
+        if (done[size_t(i)]) continue;
+        std::vector<int32_t> members;
+        for (int32_t j = i; j < n && int(members.size()) < kMaxGroup; ++j)
+            if (!done[size_t(j)] && batches[j].queries == batches[i].queries && batches[j].m == batches[i].m &&
+                batches[j].dim == batches[i].dim)
+                members.push_back(j);
+        // the costliest batch first: it sorts the shared chunks and leads each chunk
+        std::stable_sort(members.begin(), members.end(), [&](int32_t a, int32_t b) {
+            const int ka = batches[a].opt.kind == FKD_KNN ? batches[a].opt.k : 1;
+            const int kb = batches[b].opt.kind == FKD_KNN ? batches[b].opt.k : 1;
+            return ka > kb;
+        });
+        std::vector<GroupBatch> group;
+        for (int32_t j : members) {
+            fkd_host_batch* b = &batches[j];
+            GroupBatch g;
+            g.o = &b->opt;
+            g.cap2 = cap2[size_t(j)];
+            g.k = b->opt.kind == FKD_KNN ? b->opt.k : 1;
+            g.counts = b->counts;
+            g.hits = b->hits;
+            g.want_stats = b->opt.collect_stats != 0;
+            g.stats = b->stats;
+            group.push_back(g);
+            done[size_t(j)] = 1;
+        }
+        const fkd_status s = run_host_group(t, batches[i].queries, batches[i].m, batches[i].dim, group, kn);
+        for (int32_t j : members) note(&batches[j], s);
+    }
+    if (first != FKD_OK) return fail(first, first_msg);
     return FKD_OK;
 }
 

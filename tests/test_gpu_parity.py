@@ -709,3 +709,83 @@ def test_run_batches_device_concurrent_exact(oracle):
     c_ref, h_ref = torch.empty_like(c_ok), torch.empty_like(h_ok)
     fk.run_batch_device(tree, qb, c_ref, h_ref, fk.BatchOptions(kind=fk.QueryKind.knn, k=8))
     assert torch.equal(c_ok, c_ref) and torch.equal(h_ok, h_ref)
+
+
+@pytest.mark.parametrize("knobs", ["", "FKD_FULL_STAGING=0", "FKD_STREAMS=2;FKD_CHUNK_DIV=5",
+                                   "FKD_FULL_STAGING=0;FKD_STREAMS=3;FKD_BUDGET=40;FKD_RESUME_MIN=50",
+                                   "FKD_PAGEABLE_STAGING=0"])
+def test_run_batches_host_groups_exact(oracle, knobs, monkeypatch):
+    """fkd_run_batches: batches over one query array run as one pipeline
+    (shared upload, check and Morton order per chunk; full and ring device
+    staging; pageable and pinned buffers); each equals its own fkd_run_batch."""
+    import ctypes as C
+
+    for kv in filter(None, knobs.split(";")):
+        k_, v_ = kv.split("=")
+        monkeypatch.setenv(k_, v_)
+    pts = fk.clustered_points(51, 1, 80_000, 3)
+    tree = fk.KdTree.from_level_order(oracle.build_tree(pts), devices=[0, 0])
+    qa = fk.clustered_points(51, 2, 700_001, 3)
+    qb = fk.random_points(51, 3, 50_000, 3)
+    specs = [(qa, fk.BatchOptions(kind=fk.QueryKind.fcp, collect_stats=True)),
+             (qa, fk.BatchOptions(kind=fk.QueryKind.knn, k=8, collect_stats=True)),
+             (qb, fk.BatchOptions(kind=fk.QueryKind.knn, k=4)),
+             (qa, fk.BatchOptions(kind=fk.QueryKind.knn, k=20, max_radius=0.02, morton=False))]
+    got = fk.run_batches(tree, specs)
+    for (q, o), r in zip(specs, got):
+        ref = fk.run_batch(tree, q, o)
+        assert np.array_equal(r.counts, ref.counts) and r.hits.tobytes() == ref.hits.tobytes(), o
+        assert r.stats == ref.stats
+    # pinned caller buffers through the C ABI
+    m = len(qa)
+    hq = fk.LIB.fkd_host_alloc(qa.nbytes)
+    C.memmove(hq, qa.ctypes.data, qa.nbytes)
+    arr = (fk._lib.fkd_host_batch * 2)()
+    bufs = []
+    for i, o in enumerate((fk.BatchOptions(kind=fk.QueryKind.knn, k=8), fk.BatchOptions())):
+        hc, hh = fk.LIB.fkd_host_alloc(m * 4), fk.LIB.fkd_host_alloc(m * o.stride * 8)
+        bufs.append((hc, hh, o))
+        arr[i].queries, arr[i].m, arr[i].dim, arr[i].opt = hq, m, 3, o.to_c()
+        arr[i].counts, arr[i].hits, arr[i].stats = hc, hh, None
+    assert fk.LIB.fkd_run_batches(tree.handle, arr, 2) == 0, fk.LIB.fkd_last_error()
+    for hc, hh, o in bufs:
+        ref = fk.run_batch(tree, qa, o)
+        gc = np.ctypeslib.as_array(C.cast(C.c_void_p(hc), C.POINTER(C.c_int32)), shape=(m,))
+        gh = np.ctypeslib.as_array(C.cast(C.c_void_p(hh), C.POINTER(C.c_int64)), shape=(m * o.stride,))
+        assert np.array_equal(gc, ref.counts) and gh.tobytes() == ref.hits.tobytes()
+        fk.LIB.fkd_host_free(hc)
+        fk.LIB.fkd_host_free(hh)
+    fk.LIB.fkd_host_free(hq)
+
+
+def test_run_batches_rejected_group_and_many_batches(oracle):
+    """A non-finite query rejects its whole group (same queries) with the
+    first bad id and leaves pageable outputs untouched; another group's
+    batch still completes; more batches than one pipeline holds are split."""
+    import ctypes as C
+
+    tree = fk.KdTree.from_level_order(oracle.build_tree(oracle.random_points(61, 30_000, 3)))
+    bad = oracle.random_points(62, 400_000, 3)
+    bad[333_333, 0] = np.inf
+    good = oracle.random_points(63, 20_000, 3)
+    arr = (fk._lib.fkd_host_batch * 3)()
+    outs = []
+    for i, (q, o) in enumerate(((bad, fk.BatchOptions(kind=fk.QueryKind.knn, k=8)), (bad, fk.BatchOptions()),
+                                (good, fk.BatchOptions(kind=fk.QueryKind.knn, k=2)))):
+        c = np.full(len(q), -7, np.int32)
+        h = np.full(len(q) * o.stride, -7, np.int64)
+        outs.append((c, h, q, o))
+        arr[i].queries, arr[i].m, arr[i].dim, arr[i].opt = q.ctypes.data, len(q), 3, o.to_c()
+        arr[i].counts, arr[i].hits, arr[i].stats = c.ctypes.data, h.ctypes.data, None
+    assert fk.LIB.fkd_run_batches(tree.handle, arr, 3) == 2
+    assert "point 333333" in fk.LIB.fkd_last_error().decode()
+    assert [arr[i].status for i in range(3)] == [2, 2, 0]
+    for c, h, q, o in outs[:2]:
+        assert (c == -7).all() and (h == -7).all()
+    c, h, q, o = outs[2]
+    ref = fk.run_batch(tree, q, o)
+    assert np.array_equal(c, ref.counts) and h.tobytes() == ref.hits.tobytes()
+    many = [(good, fk.BatchOptions(kind=fk.QueryKind.knn, k=1 + i % 5)) for i in range(19)]
+    for (q, o), r in zip(many, fk.run_batches(tree, many)):
+        ref = fk.run_batch(tree, q, o)
+        assert np.array_equal(r.counts, ref.counts) and r.hits.tobytes() == ref.hits.tobytes()
