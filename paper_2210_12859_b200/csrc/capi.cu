@@ -54,14 +54,14 @@ int walk_bucket_of(int k);
 // The rounds run for register lists of <= 4 slots (fcp, k <= 4) and, in
 // batches of >= 2^22 queries, 8 slots (a 1M-query kNN8 batch is 4-8% slower
 // with them: the round boundaries cost more than the small batch's warps lose).
-inline bool rounds_on(int k, int64_t m) {
+inline bool rounds_on(int k, int64_t m, const Knobs& kn) {
     const int kb = walk_bucket_of(k);
-    return kb <= 4 || (kb == 8 && m >= (int64_t(1) << 22));
+    return kb <= 4 || (kb == 8 && m >= kn.rounds_min_m);
 }
 // first walk's loop trips before a query parks (FKD_BUDGET < 0: per kind)
-inline int first_budget(int k, int64_t m) {
+inline int first_budget(int k, int64_t m, const Knobs& kn) {
     if (k == 1) return 112;
-    if (!rounds_on(k, m)) return 3072;
+    if (!rounds_on(k, m, kn)) return 3072;
     return walk_bucket_of(k) <= 4 ? 256 : 384;
 }
 // resume pass trips (FKD_RESUME_TRIPS = 0): 4 x the per-kind budget without rounds
@@ -80,9 +80,9 @@ inline int resume_trips_default(int k) { return k == 1 ? 4096 : 49152; }
 // 2.49 vs 3.03 ms without it; profiles/r01i_fcp_*ab.log).
 const std::vector<int>& round_schedule(const Knobs& kn, int k, int64_t m) {
     static const std::vector<int> none;
-    if (k == 1) return (kn.rounds_fcp_env || m >= (int64_t(1) << 22)) ? kn.rounds_fcp : kn.rounds_fcp_small;
+    if (k == 1) return (kn.rounds_fcp_env || m >= kn.rounds_min_m) ? kn.rounds_fcp : kn.rounds_fcp_small;
     if (kn.rounds_knn_all) return kn.rounds_knn_env;
-    if (!rounds_on(k, m)) return none;
+    if (!rounds_on(k, m, kn)) return none;
     return walk_bucket_of(k) <= 4 ? kn.rounds_knn4 : kn.rounds_knn8;
 }
 
@@ -609,7 +609,7 @@ fkd_status enqueue(const fkd_tree* t, Replica& r, Workspace* w, const float* d_q
         a.per_query = d_per_query ? d_per_query + base : nullptr;
         a.bad = w->small;
         a.id_base = id_offset + base;
-        int budget = tu.budget >= 0 ? tu.budget : first_budget(k, cm);
+        int budget = tu.budget >= 0 ? tu.budget : first_budget(k, cm, tu);
         if (budget_div > 1 && budget > 0) budget = std::max(64, budget / budget_div);
         a.budget = (stats || walk_bucket_of(k) == 0 || t->dim > 8) ? 0 : budget;
         if (a.budget > 0) {
@@ -1369,6 +1369,7 @@ struct DevicePipe {
     size_t r_slot_bytes = 0;
     std::vector<cudaEvent_t> ev_in;                    // per chunk
     std::vector<cudaEvent_t> ev_sorted, ev_walk, ev_out;  // per job
+    cudaEvent_t ev_start = nullptr;                       // FKD_PIPE_TRACE
     // enqueue thread -> drain thread hand-off
     std::mutex mu;
     std::condition_variable cv;
@@ -1551,8 +1552,13 @@ fkd_status run_host_group(const fkd_tree* t, const float* queries, int64_t m, in
         for (auto* v : {&P->ev_sorted, &P->ev_walk, &P->ev_out}) v->assign(P->jobs.size(), nullptr);
         for (auto* v : {&P->ev_in, &P->ev_sorted, &P->ev_walk, &P->ev_out})
             for (auto& e : *v)
-                if (err == FKD_OK && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
+                if (err == FKD_OK && cudaEventCreateWithFlags(&e, kn.pipe_trace ? cudaEventDefault : cudaEventDisableTiming) !=
+                                         cudaSuccess)
                     err = fail(FKD_CUDA_ERROR, "event create failed");
+        if (kn.pipe_trace && err == FKD_OK) {
+            cudaEventCreate(&P->ev_start);
+            cudaEventRecord(P->ev_start, P->wss[0]->cin);
+        }
         for (Workspace* w : P->wss) {
             cudaError_t e = reset_small(w, w->stream);
             if (e != cudaSuccess && err == FKD_OK) err = fail(FKD_CUDA_ERROR, std::string("reset: ") + cudaGetErrorString(e));
@@ -1788,6 +1794,17 @@ fkd_status run_host_group(const fkd_tree* t, const float* queries, int64_t m, in
         }
         if (err == FKD_OK)
             for (int i = 0; i < 3 * B; ++i) tot[size_t(i)] += P->wss[0]->h_small[kBatchTotals + i];
+        if (P->ev_start && err == FKD_OK) {  // FKD_PIPE_TRACE: per-job timeline, ms from the first H2D
+            for (size_t j = 0; j < P->jobs.size(); ++j) {
+                float tin = 0, tw = 0, tout = 0;
+                cudaEventElapsedTime(&tin, P->ev_start, P->ev_in[size_t(P->jobs[j].chunk)]);
+                cudaEventElapsedTime(&tw, P->ev_start, P->ev_walk[j]);
+                cudaEventElapsedTime(&tout, P->ev_start, P->ev_out[j]);
+                std::fprintf(stderr, "dev %d job %zu chunk %d batch %d n=%lld h2d_end %.3f walk_end %.3f d2h_end %.3f\n",
+                             P->di, j, P->jobs[j].chunk, P->jobs[j].b, (long long)P->jobs[j].count, tin, tw, tout);
+            }
+            cudaEventDestroy(P->ev_start);
+        }
         for (Workspace* w : P->wss) release_ws(*P->rep, w);
         for (auto* v : {&P->ev_in, &P->ev_sorted, &P->ev_walk, &P->ev_out})
             for (auto& e : *v)

@@ -24,6 +24,7 @@ std::vector<int> parse_ints(const char* e) {
 Knobs read_knobs() {
     Knobs k;
     if (const char* e = std::getenv("FKD_BUDGET")) k.budget = std::atoi(e);
+    if (const char* e = std::getenv("FKD_ROUNDS_MIN_M")) k.rounds_min_m = std::atoll(e);
     if (const char* e = std::getenv("FKD_RESUME_MIN")) k.resume_min = std::atoll(e);
     if (const char* e = std::getenv("FKD_RESUME_TRIPS")) k.resume_trips = std::atoi(e);
     if (const char* e = std::getenv("FKD_RROUNDS_FCP")) {
@@ -43,6 +44,7 @@ Knobs read_knobs() {
     if (const char* e = std::getenv("FKD_FULL_STAGING")) k.full_staging = std::atoi(e) != 0;
     if (const char* e = std::getenv("FKD_PAGEABLE_STAGING")) k.pageable_staging = std::atoi(e) != 0;
     if (const char* e = std::getenv("FKD_HOST_RING")) k.host_ring = std::max(1, std::atoi(e));
+    if (const char* e = std::getenv("FKD_PIPE_TRACE")) k.pipe_trace = std::atoi(e) != 0;
     return k;
 }
 

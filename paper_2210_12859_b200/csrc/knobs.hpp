@@ -9,6 +9,7 @@
 //   FKD_BUDGET           first walk's loop trips before a query parks (<0 per kind, 0 off)
 //   FKD_RROUNDS_FCP      continuation-round trips for fcp, "t1,t2,.." ("0": none)
 //   FKD_RROUNDS_KNN      continuation-round trips for every kNN bucket
+//   FKD_ROUNDS_MIN_M     batch size from which 8-slot lists take rounds and fcp a third round (2^22)
 //   FKD_RESUME_MIN       parked walks that select the plain-grid resume pass (0: SMs x 64)
 //   FKD_RESUME_TRIPS     trips the resume pass adds before the CTA pass (0: per kind, <0 unbounded)
 //   FKD_CHUNK            host path: uniform chunk size instead of the graduated schedule
@@ -19,6 +20,7 @@
 //   FKD_FULL_STAGING     host path: 0 forces the device-side ring staging
 //   FKD_PAGEABLE_STAGING host path: 0 hands pageable caller buffers to cudaMemcpyAsync
 //   FKD_HOST_RING        host path: pinned staging slots per direction per device (4)
+//   FKD_PIPE_TRACE       host path: 1 prints each job's H2D / walk / D2H end times (stderr)
 //
 // Experiments that were measured and settled are compile-time constants
 // (store layout, node shift, carveout, Morton bits, sort thresholds, CTA-pass
@@ -40,6 +42,7 @@ struct Knobs {
     bool rounds_fcp_env = false;  // FKD_RROUNDS_FCP given: every batch size
     std::vector<int> rounds_knn_env;
     bool rounds_knn_all = false;  // FKD_RROUNDS_KNN given: every kNN bucket
+    int64_t rounds_min_m = int64_t(1) << 22;
     int64_t resume_min = 0;
     int resume_trips = 0;
     // host pipeline
@@ -51,6 +54,7 @@ struct Knobs {
     bool full_staging = true;
     bool pageable_staging = true;
     int host_ring = 4;
+    bool pipe_trace = false;
 };
 
 // A snapshot of the environment overrides on top of the defaults.

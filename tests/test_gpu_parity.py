@@ -789,3 +789,26 @@ def test_run_batches_rejected_group_and_many_batches(oracle):
     for (q, o), r in zip(many, fk.run_batches(tree, many)):
         ref = fk.run_batch(tree, q, o)
         assert np.array_equal(r.counts, ref.counts) and r.hits.tobytes() == ref.hits.tobytes()
+
+
+def test_bench_matrix_csv_matches_reference(reference):
+    """bench_matrix.write_bench_csv (bench.cpp:119-133 schema) on the B200
+    path against the reference's own run_bench_matrix + write_bench_csv on
+    the same seeds: identical rows except engine/threads and the timings."""
+    import io
+
+    from paper_2210_12859_b200 import bench_matrix as bm
+
+    for kind, ks, rs in (("fcp", (8,), (INF,)), ("knn", (1, 8, 20), (INF, 0.05))):
+        base = bm.BenchConfig(n_queries=20_000, k_dim=3, kind=fk.QueryKind[kind], reps=2)
+        rows = bm.run_bench_matrix(base, [1000, 7000], ks, rs)
+        buf = io.StringIO()
+        bm.write_bench_csv(buf, rows)
+        ours = [line.split(",") for line in buf.getvalue().strip().splitlines()]
+        ref = [line.split(",") for line in
+               reference.bench_matrix_csv(20_000, 3, kind, 2, [1000, 7000], ks, rs).strip().splitlines()]
+        assert ours[0] == ref[0] and len(ours) == len(ref)
+        keep = [0, 1, 2, 3, 6, 7, 10, 11, 12]  # n query k max_r reps total nodes/q steps/q hash
+        for a, b in zip(ours[1:], ref[1:]):
+            assert [a[i] for i in keep] == [b[i] for i in keep], (a, b)
+            assert a[4] == "b200" and b[4] == "stackfree"

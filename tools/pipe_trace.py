@@ -1,16 +1,27 @@
-"""One C3 kNN8 / fcp host-path call with FKD_PIPE_TRACE=1 (per-chunk timeline on stderr)."""
-import ctypes as C, os, sys
+"""Per-job timeline of one C3 host-path call (FKD_PIPE_TRACE=1): fcp + kNN8
+grouped (fkd_run_batches) with pinned buffers.  Usage: python tools/pipe_trace.py [knobs...]"""
+import ctypes as C
+import os
+import sys
+
+import numpy as np
+
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import paper_2210_12859_b200 as fk
+import paper_2210_12859_b200 as fk  # noqa: E402
+
 m, dim = 10_000_000, 3
 tree = fk.build_tree(fk.clustered_points(1, 1, m, dim))
 qs = fk.clustered_points(1, 2, m, dim)
-hq = fk.LIB.fkd_host_alloc(qs.nbytes); C.memmove(hq, qs.ctypes.data, qs.nbytes)
-for kind, k in (("fcp", 1), ("knn", 8)):
-    hc = fk.LIB.fkd_host_alloc(m * 4); hh = fk.LIB.fkd_host_alloc(m * k * 8)
-    o = fk.BatchOptions(kind=fk.QueryKind[kind], k=k).to_c()
-    for rep in range(3):
-        if rep == 2: os.environ["FKD_PIPE_TRACE"] = "1"; print(kind, flush=True)
-        fk.LIB.fkd_run_batch(tree.handle, hq, m, dim, C.byref(o), hc, hh, None)
-        sys.stderr.flush()
-    os.environ.pop("FKD_PIPE_TRACE", None)
+hq = fk.LIB.fkd_host_alloc(qs.nbytes)
+C.memmove(hq, qs.ctypes.data, qs.nbytes)
+arr = (fk._lib.fkd_host_batch * 2)()
+for i, o in enumerate((fk.BatchOptions(kind=fk.QueryKind.knn, k=8), fk.BatchOptions())):
+    arr[i].queries, arr[i].m, arr[i].dim, arr[i].opt = hq, m, dim, o.to_c()
+    arr[i].counts, arr[i].hits = fk.LIB.fkd_host_alloc(m * 4), fk.LIB.fkd_host_alloc(m * o.stride * 8)
+for kv in sys.argv[1:]:
+    k, v = kv.split("=")
+    os.environ[k] = v
+for rep in range(3):
+    if rep == 2:
+        os.environ["FKD_PIPE_TRACE"] = "1"
+    assert fk.LIB.fkd_run_batches(tree.handle, arr, 2) == 0
