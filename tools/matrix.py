@@ -22,7 +22,19 @@ import paper_2210_12859_b200 as fk  # noqa: E402
 from oracle import Reference  # noqa: E402
 
 INF = float("inf")
-HBM = 6543.7
+
+
+def _hbm_peak() -> float:
+    """Measured HBM GB/s (MEASURED_PEAKS.json, driver-written), else the
+    B200_PROFILING.md fallback."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"])
+    except Exception:
+        return 6650.0
+
+
+HBM = _hbm_peak()
 
 
 def gen(kind, stream, count, dim):
