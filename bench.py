@@ -289,7 +289,7 @@ def run_b200(args) -> None:
     import torch
 
     import paper_2210_12859_b200 as fk
-    from paper_2210_12859_b200.shard import max_over_ranks, replicate_tree, shard_range
+    from paper_2210_12859_b200.shard import MortonExchange, max_over_ranks, replicate_tree, shard_range
 
     world, rank, local = dist_env()
     dist = None
@@ -345,6 +345,24 @@ def run_b200(args) -> None:
         concurrently, the costliest at the highest stream priority, sharing
         one Morton order of the common query array); --serial: back-to-back
         fkd_run_batch_device calls."""
+        if args.partition == "morton" and world > 1:
+            # Morton-range partition (SURVEY §8(e)): keys, histogram
+            # all-reduce, all-to-all of the queries, the local walk of this
+            # rank's key range, all-to-all of the answers back to their slots
+            keys, kbits = fk.morton_keys(tree, qs_dev, stream=stream)
+            ex = MortonExchange(qs_dev, keys, kbits, world)
+            local = []
+            for (kind, k, _), o in zip(batches, opts):
+                lm = ex.local_queries.shape[0]
+                local.append((torch.empty(lm, dtype=torch.int32, device=dev),
+                              torch.empty(lm * k, dtype=torch.int64, device=dev)))
+            res = fk.run_batches_device(tree, [(ex.local_queries, c, h, o) for (c, h), o in zip(local, opts)],
+                                        stream=stream, timings=timing)
+            for (kind, k, _), (c, h) in zip(batches, local):
+                rc, rh = ex.return_results(c, h, k)
+                outs[(kind, k)][0].copy_(rc)
+                outs[(kind, k)][1].copy_(rh)
+            return [tm for _, tm in res]
         if args.serial:
             tms = []
             for (kind, k, _), o in zip(batches, opts):
@@ -543,6 +561,7 @@ def run_b200(args) -> None:
             "unit": "warp-instructions/s", "kernel": "walk knn8",
             "source": "instruction count per launch from profiles/traffic.json (ncu), time live"},
         "per_batch": per_batch,
+        "partition": (args.partition if world > 1 else "single GPU"),
         "submission": ("serial: one fkd_run_batch_device call per batch" if args.serial else
                        "one fkd_run_batches_device call per step: the batches run concurrently (costliest at "
                        "the highest stream priority) and share one Morton order of the common query array"),
@@ -577,6 +596,9 @@ def main():
                     help="queries per batch of the reference arm (same rule as --cpu-sample)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-pageable", action="store_true", help="skip the e2e_pageable measurement")
+    ap.add_argument("--partition", choices=["block", "morton"], default="block",
+                    help="multi-GPU query partition: contiguous blocks (no data-path collective) or Morton "
+                         "key ranges (histogram all-reduce + two all-to-alls per step)")
     ap.add_argument("--serial", action="store_true",
                     help="submit the step's batches as back-to-back calls instead of one concurrent submission")
     args = ap.parse_args()

@@ -118,6 +118,13 @@ int32_t fkd_tree_dim(const fkd_tree* tree);
  * fkd_run_batch_device runs on the first one. */
 int32_t fkd_tree_replicas(const fkd_tree* tree, int32_t* devices, int32_t cap);
 
+/* Morton keys of device queries over the tree's bounding box (the key the
+ * batch ordering uses, at full resolution: *key_bits = bits per axis x dim,
+ * <= 24), for partitioning a batch across GPUs by key range
+ * (paper_2210_12859_b200/shard.py).  Rejects non-finite queries. */
+fkd_status fkd_morton_keys(const fkd_tree* tree, const float* d_queries, int64_t m, int32_t dim,
+                           uint32_t* d_keys, int32_t* key_bits, void* stream);
+
 /* Adds replicas of the tree store on `devices` (appended to the shard
  * order), copied device to device from the existing replicas as a pipelined
  * chain over NVLink / NVSwitch (64 MB pieces; cudaMemcpyPeerAsync staging

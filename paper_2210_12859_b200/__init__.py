@@ -41,7 +41,7 @@ __all__ = [
     "BatchOptions", "BatchResult", "DataError", "DeviceError", "Engine", "HIT_DTYPE",
     "InvalidArgument", "InvariantError", "KdTree", "QueryKind", "QueryStats", "build_tree",
     "build_level_order", "build_level_order_device", "clustered_points", "fcp", "knn", "random_points", "result_hash", "run_batch",
-    "run_batch_device", "run_batches", "run_batches_device", "write_query_results", "LIB_PATH",
+    "run_batch_device", "run_batches", "run_batches_device", "morton_keys", "write_query_results", "LIB_PATH",
 ]
 
 HIT_DTYPE = np.dtype([("node", "<i4"), ("dist2", "<f4")])  # flatkd::Hit, 8 bytes
@@ -431,6 +431,24 @@ def run_batches_device(tree: KdTree, batches, stream=None, timings: bool = False
         stream = torch.cuda.current_stream(batches[0][0].device)
     _check(LIB.fkd_run_batches_device(tree.handle, arr, n, _stream_ptr(stream)))
     return [(QueryStats.from_c(st), _timings_dict(tm) if timings else None) for st, tm, _ in keep]
+
+
+def morton_keys(tree: KdTree, queries, stream=None):
+    """Morton keys of device queries over the tree's bounding box (the batch
+    ordering's key at full resolution) -> (uint32-valued int64 tensor, key
+    bits); the multi-GPU Morton-range partition splits batches by them."""
+    import torch
+
+    if not queries.is_cuda or queries.dtype != torch.float32 or queries.dim() != 2 or not queries.is_contiguous():
+        raise DataError("queries: expected a contiguous CUDA float32 (m, dim) tensor")
+    m, dim = queries.shape
+    keys = torch.empty(m, dtype=torch.int32, device=queries.device)
+    bits = C.c_int32(0)
+    if stream is None:
+        stream = torch.cuda.current_stream(queries.device)
+    _check(LIB.fkd_morton_keys(tree.handle, C.c_void_p(queries.data_ptr()), m, dim, C.c_void_p(keys.data_ptr()),
+                               C.byref(bits), _stream_ptr(stream)))
+    return keys.to(torch.int64) & 0xFFFFFFFF, int(bits.value)
 
 
 def fcp(tree: KdTree, query, max_radius: float = INF, stats: bool = False):

@@ -764,6 +764,32 @@ void fkd_host_free(void* p) { cudaFreeHost(p); }
 int64_t fkd_tree_size(const fkd_tree* t) { return t ? t->n : 0; }
 int32_t fkd_tree_dim(const fkd_tree* t) { return t ? t->dim : 0; }
 
+fkd_status fkd_morton_keys(const fkd_tree* t, const float* d_queries, int64_t m, int32_t dim, uint32_t* d_keys,
+                           int32_t* key_bits, void* stream) {
+    if (!t) return fail(FKD_INVALID_ARGUMENT, "null tree");
+    if (key_bits) *key_bits = t->n > 0 && t->dim <= 8 ? t->frame.bits * t->dim : 0;
+    if (m < 0) return fail(FKD_INVALID_ARGUMENT, "negative query count");
+    if (m == 0 || t->n == 0) return FKD_OK;
+    if (dim != t->dim)
+        return fail(FKD_DATA_ERROR, "query dimension " + std::to_string(dim) + " does not match tree dimension " +
+                                        std::to_string(t->dim));
+    if (t->dim > 8) return fail(FKD_INVALID_ARGUMENT, "Morton keys exist for dim <= 8");
+    if (t->reps.empty()) return fail(FKD_NO_DEVICE, "tree has no device replica");
+    DeviceGuard g(t->reps[0]->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    unsigned long long* bad = nullptr;
+    FKD_CUDA(cudaMallocAsync(&bad, sizeof(unsigned long long), st));
+    FKD_CUDA(cudaMemsetAsync(bad, 0xFF, sizeof(unsigned long long), st));
+    if (morton_keys(d_queries, m, dim, t->frame, d_keys, bad, st) < 0) return fail(FKD_CUDA_ERROR, "morton keys");
+    FKD_CUDA(cudaGetLastError());
+    unsigned long long h = 0;
+    FKD_CUDA(cudaMemcpyAsync(&h, bad, sizeof(h), cudaMemcpyDeviceToHost, st));
+    FKD_CUDA(cudaFreeAsync(bad, st));
+    FKD_CUDA(cudaStreamSynchronize(st));
+    if (h != kNoBad) return fail(FKD_DATA_ERROR, "queries: non-finite coordinate in point " + std::to_string(h));
+    return FKD_OK;
+}
+
 int32_t fkd_tree_replicas(const fkd_tree* t, int32_t* devices, int32_t cap) {
     if (!t) return 0;
     const int32_t n = int32_t(t->reps.size());

@@ -124,6 +124,30 @@ __global__ void __launch_bounds__(256)
     ids[i] = uint32_t(i);
 }
 
+// keys only (full frame resolution, no sort): the multi-GPU Morton-range
+// partition (paper_2210_12859_b200/shard.py) splits a batch by these keys
+template <int D>
+__global__ void __launch_bounds__(256)
+    morton_keys_only_kernel(const float* __restrict__ q, int64_t m, MortonFrame f, uint32_t* __restrict__ keys,
+                            unsigned long long* bad) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    keys[i] = morton_key<D>(q, i, f, bad, 0);
+}
+
+int morton_keys(const float* d_queries, int64_t m, int dim, const MortonFrame& f, uint32_t* keys,
+                unsigned long long* bad, cudaStream_t st) {
+    if (m <= 0) return 0;
+    const unsigned grid = unsigned((m + 255) / 256);
+    switch (dim) {
+#define FKD_KEYS(D) case D: morton_keys_only_kernel<D><<<grid, 256, 0, st>>>(d_queries, m, f, keys, bad); break;
+        FKD_KEYS(1) FKD_KEYS(2) FKD_KEYS(3) FKD_KEYS(4) FKD_KEYS(5) FKD_KEYS(6) FKD_KEYS(7) FKD_KEYS(8)
+#undef FKD_KEYS
+        default: return -1;
+    }
+    return 1;
+}
+
 size_t morton_temp_bytes(int64_t m, int dim) {
     size_t bytes = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr,

@@ -22,6 +22,9 @@ size_t morton_temp_bytes(int64_t m, int dim);
 int morton_order(const float* d_queries, int64_t m, int dim, const MortonFrame& f,
                  uint32_t* keys_in, uint32_t* keys_out, uint32_t* ids_in, uint32_t* ids_out,
                  void* temp, size_t temp_bytes, unsigned long long* bad, int64_t id_base, cudaStream_t st);
+// Morton keys only (frame resolution, f.bits per axis), first non-finite id -> *bad.
+int morton_keys(const float* d_queries, int64_t m, int dim, const MortonFrame& f, uint32_t* keys,
+                unsigned long long* bad, cudaStream_t st);
 // First non-finite query (id_base + i) -> *bad, for batches walked without the key pass.
 int scan_queries(const float* d_queries, int64_t m, int dim, unsigned long long* bad, int64_t id_base,
                  cudaStream_t st);

@@ -812,3 +812,39 @@ def test_bench_matrix_csv_matches_reference(reference):
         for a, b in zip(ours[1:], ref[1:]):
             assert [a[i] for i in keep] == [b[i] for i in keep], (a, b)
             assert a[4] == "b200" and b[4] == "stackfree"
+
+
+def test_morton_keys_and_exchange_single_rank(oracle):
+    """fkd_morton_keys = the batch ordering's key over the tree's box (24
+    bits); the Morton-range exchange at world size 1 is the identity and the
+    walk over its local queries returns the unpartitioned answer."""
+    import torch
+
+    from paper_2210_12859_b200.shard import MortonExchange
+
+    nodes = oracle.build_tree(oracle.random_points(71, 50_000, 3))
+    tree = fk.KdTree.from_level_order(nodes)
+    qs = oracle.random_points(72, 30_000, 3) * np.float32(1.2) - np.float32(0.1)
+    q = torch.from_numpy(qs).cuda()
+    keys, bits = fk.morton_keys(tree, q)
+    assert bits == 24
+    lo, hi = nodes.min(0), nodes.max(0)
+    top = np.float32((1 << 8) - 1)
+    scale = (np.float64(top) / (hi.astype(np.float64) - lo.astype(np.float64))).astype(np.float32)
+    t = np.minimum(np.maximum((qs - lo) * scale, np.float32(0)), top).astype(np.int64)
+    ref = np.zeros(len(qs), np.int64)
+    for b in range(7, -1, -1):
+        for d in range(3):
+            ref = (ref << 1) | ((t[:, d] >> b) & 1)
+    assert np.array_equal(keys.cpu().numpy(), ref)
+    ex = MortonExchange(q, keys, bits, 1)
+    c = torch.empty(len(qs), dtype=torch.int32, device="cuda")
+    h = torch.empty(len(qs) * 8, dtype=torch.int64, device="cuda")
+    fk.run_batch_device(tree, ex.local_queries, c, h, fk.BatchOptions(kind=fk.QueryKind.knn, k=8))
+    rc, rh = ex.return_results(c, h, 8)
+    ref_c, ref_h, _, _ = oracle.run_batch(nodes, qs, "knn", 8)
+    assert np.array_equal(rc.cpu().numpy(), ref_c) and rh.cpu().numpy().tobytes() == ref_h.tobytes()
+    bad = q.clone()
+    bad[17, 1] = float("nan")
+    with pytest.raises(fk.DataError, match="point 17"):
+        fk.morton_keys(tree, bad)
