@@ -54,15 +54,15 @@ void launch_one(const WalkArgs& a, cudaStream_t st) {
 }
 
 template <int D, int S, int KB>
-void launch_coop(const WalkArgs& a, cudaStream_t st) {
-    auto kernel = walk_coop_kernel<D, S, KB>;
-    constexpr size_t smem = coop_smem_bytes<KB>();
+void launch_smheap(const WalkArgs& a, cudaStream_t st) {
+    auto kernel = walk_smheap_kernel<D, S, KB>;
+    constexpr size_t smem = smheap_bytes<KB>();
     static const bool attr = [&] {
         cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         return true;
     }();
     (void)attr;
-    kernel<<<walk_blocks(a.m, coop_threads<KB>()), coop_threads<KB>(), smem, st>>>(a);
+    kernel<<<walk_blocks(a.m, smheap_threads<KB>()), smheap_threads<KB>(), smem, st>>>(a);
 }
 
 template <int D, int S, int KB, bool UNORDERED>
@@ -87,8 +87,8 @@ int launch_bucket(const WalkArgs& a, bool stats, bool unordered, int phase, cuda
         return 1;
     }
     if constexpr (KB >= 16) {
-        if (a.coop && !stats && !unordered) {
-            launch_coop<D, S, KB>(a, st);
+        if (a.smheap && !stats && !unordered) {
+            launch_smheap<D, S, KB>(a, st);
             return 1;
         }
     }
