@@ -612,10 +612,6 @@ fkd_status enqueue(const fkd_tree* t, Replica& r, Workspace* w, const float* d_q
         int budget = tu.budget >= 0 ? tu.budget : first_budget(k, cm, tu);
         if (budget_div > 1 && budget > 0) budget = std::max(64, budget / budget_div);
         a.budget = (stats || walk_bucket_of(k) == 0 || t->dim > 8) ? 0 : budget;
-        // lists of >= smheap_min_k slots: the shared-memory heap walk
-        // (walk_smheap_kernel), except the 8-D 16-slot output-slot list
-        a.smheap = tu.smheap_min_k > 0 && walk_bucket_of(k) >= tu.smheap_min_k && t->dim <= 8 &&
-                 !(t->dim >= 8 && walk_bucket_of(k) == 16) && !stats && !(o->flags & FKD_FLAG_UNORDERED);
         if (a.budget > 0) {
             FKD_CUDA(grow(w->ovf, w->ovf_cap, cm));
             FKD_CUDA(grow(w->wave_state, w->wave_state_cap, cm));

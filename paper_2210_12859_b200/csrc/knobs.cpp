@@ -25,7 +25,6 @@ Knobs read_knobs() {
     Knobs k;
     if (const char* e = std::getenv("FKD_BUDGET")) k.budget = std::atoi(e);
     if (const char* e = std::getenv("FKD_ROUNDS_MIN_M")) k.rounds_min_m = std::atoll(e);
-    if (const char* e = std::getenv("FKD_SMHEAP_MIN_K")) k.smheap_min_k = std::max(0, std::atoi(e));
     if (const char* e = std::getenv("FKD_RESUME_MIN")) k.resume_min = std::atoll(e);
     if (const char* e = std::getenv("FKD_RESUME_TRIPS")) k.resume_trips = std::atoi(e);
     if (const char* e = std::getenv("FKD_RROUNDS_FCP")) {

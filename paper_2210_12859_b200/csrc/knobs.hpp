@@ -10,7 +10,6 @@
 //   FKD_RROUNDS_FCP      continuation-round trips for fcp, "t1,t2,.." ("0": none)
 //   FKD_RROUNDS_KNN      continuation-round trips for every kNN bucket
 //   FKD_ROUNDS_MIN_M     batch size from which 8-slot lists take rounds and fcp a third round (2^22)
-//   FKD_SMHEAP_MIN_K     smallest list bucket walked with the shared-memory heap (0: off)
 //   FKD_RESUME_MIN       parked walks that select the plain-grid resume pass (0: SMs x 64)
 //   FKD_RESUME_TRIPS     trips the resume pass adds before the CTA pass (0: per kind, <0 unbounded)
 //   FKD_CHUNK            host path: uniform chunk size instead of the graduated schedule
@@ -44,7 +43,6 @@ struct Knobs {
     std::vector<int> rounds_knn_env;
     bool rounds_knn_all = false;  // FKD_RROUNDS_KNN given: every kNN bucket
     int64_t rounds_min_m = int64_t(1) << 22;
-    int smheap_min_k = 20;
     int64_t resume_min = 0;
     int resume_trips = 0;
     // host pipeline

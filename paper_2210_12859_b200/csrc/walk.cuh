@@ -70,7 +70,6 @@ struct WalkArgs {
     int2* wave_state;                      // [m] (curr, prev) of suspended walks
     int64_t resume_min;                    // >= this many over-budget queries: resume them with
                                            // the plain grid instead of the CTA overflow pass
-    int32_t smheap;                        // first walk: shared-memory heap list (walk_smheap_kernel)
 };
 
 __device__ __forceinline__ uint64_t make_key(float d2, int32_t node) {
@@ -288,7 +287,7 @@ __device__ __forceinline__ int dim_down(int d) {  // split dim one level up
 #define FKD_STREAM_IO_MIN_KB 8
 #endif
 
-template <int D, int S, int KB, bool STATS, bool UNORDERED, bool SMHEAP = false>
+template <int D, int S, int KB, bool STATS, bool UNORDERED>
 struct LaneWalk {
     // With a split-plane slot in the store (S > D) the walk never needs the
     // split dimension: qr holds the query rotated so that qr[0] is the
@@ -302,18 +301,10 @@ struct LaneWalk {
     // a register.  In 8-D a query processes ~15k nodes for ~100 admissions,
     // so the 32 list registers buy nothing but cost occupancy in a walk that
     // is load-latency bound.
-    static constexpr bool kSlot = !SMHEAP && D >= FKD_SLOT_LIST_MIN_D && KB == 16;
-    // Shared-memory heap mode (walk_smheap_kernel): the candidates form the
-    // reference's bounded max-heap (KnnCandidates, traverse.hpp:113-175) in
-    // shared memory, element e of this lane at hp[32 e] (lanes interleaved,
-    // so a warp's accesses to one level never conflict); L[0] is the kth key
-    // (the cap key while fewer than k are held, then the heap top).
-    static constexpr bool kHeap = SMHEAP;
+    static constexpr bool kSlot = D >= FKD_SLOT_LIST_MIN_D && KB == 16;
     float q[D];
     float qr[kRot ? D : 1];
-    uint64_t L[(kSlot || kHeap) ? 1 : KB];  // slot / heap mode: L[0] is the kth key
-    uint64_t* hp;                           // heap mode: this lane's element 0
-    int held;                               // heap mode: elements held
+    uint64_t L[kSlot ? 1 : KB];  // slot mode: L[0] is the kth key
     int32_t curr, prev;
     int d;  // split dim of curr, tracked incrementally (tree.hpp:27-29)
     float r2;
@@ -346,10 +337,7 @@ struct LaneWalk {
             for (int j = 0; j < D; ++j) qr[j] = q[j];  // depth 0 splits dim 0
         }
         const uint64_t empty = cap_key(a.cap2);
-        if constexpr (kHeap) {
-            L[0] = empty;
-            held = 0;
-        } else if constexpr (kSlot) {
+        if constexpr (kSlot) {
             int2* out = reinterpret_cast<int2*>(a.hits + qi * a.k);
             for (int j = 0; j < a.k; ++j) out[j] = make_int2(-1, 0x7f800000);  // Hit{-1, +inf}
             L[0] = empty;
@@ -400,12 +388,7 @@ struct LaneWalk {
             // admission is predicated on a first visit.
             const float d2 = sq_dist<D, (D <= 4 && KB <= 8)>(q, p);
             const uint64_t key = make_key(d2, curr);
-            if constexpr (kHeap) {
-                if (from_parent && key_lt(key, L[0])) {  // d2 <= cap2 and beats the kth (traverse.hpp:121-131)
-                    heap_add(a.k, key);
-                    r2 = key_dist(L[0]);
-                }
-            } else if constexpr (kSlot) {
+            if constexpr (kSlot) {
                 if (from_parent && key_lt(key, L[0])) {
                     slot_insert(a, key);
                     r2 = key_dist(L[0]);
@@ -417,12 +400,7 @@ struct LaneWalk {
         } else if (from_parent) {  // fcp, D != 3: a branch is cheaper than the FP ops
             const float d2 = sq_dist<D, (D <= 4 && KB <= 8)>(q, p);
             const uint64_t key = make_key(d2, curr);
-            if constexpr (kHeap) {
-                if (key_lt(key, L[0])) {
-                    heap_add(a.k, key);
-                    r2 = key_dist(L[0]);
-                }
-            } else if constexpr (kSlot) {
+            if constexpr (kSlot) {
                 if (key_lt(key, L[0])) {
                     slot_insert(a, key);
                     r2 = key_dist(L[0]);
@@ -495,84 +473,6 @@ struct LaneWalk {
         prev = curr;
         curr = next;
         return true;
-    }
-
-    // Heap mode: push while fewer than k are held (sift up), else replace the
-    // top (sift down) — KnnCandidates::consider (traverse.hpp:121-131) with
-    // hit_order as the key order (keys are distinct: node ids are).  Depths
-    // are bounded by the compile-time bucket, so the loops unroll into
-    // predicated levels.  L[0] becomes the heap top once the heap is full.
-    static constexpr int kHeapLevels = KB <= 1 ? 1 : 32 - __builtin_clz(unsigned(KB));  // ceil(log2(KB+1))
-    __device__ __forceinline__ void heap_add(int k, uint64_t x) {
-        if (held < k) {
-            int i = held++;
-            bool up = true;
-#pragma unroll
-            for (int l = 0; l < kHeapLevels; ++l) {
-                if (up && i > 0) {
-                    const int par = (i - 1) >> 1;
-                    const uint64_t pk = hp[32 * par];
-                    if (key_lt(pk, x)) {
-                        hp[32 * i] = pk;
-                        i = par;
-                    } else {
-                        up = false;
-                    }
-                }
-            }
-            hp[32 * i] = x;
-            if (held == k) L[0] = hp[0];
-        } else {
-            sift_down(x, k);
-            L[0] = hp[0];
-        }
-    }
-    // places x at the top of the heap [0, end) and sifts it down
-    __device__ __forceinline__ void sift_down(uint64_t x, int end) {
-        int i = 0;
-        bool down = true;
-#pragma unroll
-        for (int l = 0; l < kHeapLevels; ++l) {
-            const int c = 2 * i + 1;
-            if (down && c < end) {
-                uint64_t ck = hp[32 * c];
-                int m = c;
-                if (c + 1 < end) {
-                    const uint64_t rk = hp[32 * (c + 1)];
-                    if (key_lt(ck, rk)) {
-                        ck = rk;
-                        m = c + 1;
-                    }
-                }
-                if (key_lt(x, ck)) {
-                    hp[32 * i] = ck;
-                    i = m;
-                } else {
-                    down = false;
-                }
-            } else {
-                down = false;
-            }
-        }
-        hp[32 * i] = x;
-    }
-    // Heap mode: heap-sort in place (extract_sorted, traverse.cpp:18-23) and
-    // write the fixed-stride slot ascending, Hit{-1, +inf} past the hits; a
-    // parked walk leaves the same sorted partial list for the later passes.
-    __device__ __forceinline__ void heap_finish(const WalkArgs& a, bool final) {
-        const int k = a.k;
-        for (int end = held - 1; end > 0; --end) {
-            const uint64_t top = hp[0];
-            const uint64_t x = hp[32 * end];
-            hp[32 * end] = top;
-            sift_down(x, end);
-        }
-        int2* out = reinterpret_cast<int2*>(a.hits + qi * k);
-        for (int j = 0; j < k; ++j) {
-            const uint64_t key = j < held ? hp[32 * j] : kEmptyKey;
-            __stcs(out + j, make_int2(int32_t(uint32_t(key)), int32_t(uint32_t(key >> 32) - 1u)));
-        }
-        if (final) __stcs(a.counts + qi, held);
     }
 
     // Sorted insertion into the output slot (slot mode): x passes the
@@ -857,47 +757,6 @@ __global__ void __launch_bounds__(kWalkThreads, walk_min_blocks<D, KB>()) walk_r
         if (lane == leader) base = atomicAdd(a.wave_n_out, (unsigned long long)__popc(mask));
         base = __shfl_sync(0xffffffffu, base, leader);
         if (park) a.wave_out[base + __popc(mask & ((1u << lane) - 1u))] = qid;
-    }
-}
-
-// ---------------------------------------------------------------------------
-// Shared-memory heap walk for long lists (k of 20-64).  ncu of the 4-D kNN50
-// register-list walk (profiles/r02/r02p_*): the sorted insertion (DSETP +
-// SEL pairs, ~150 SASS for 50 slots) is 52% of all warp instructions and runs
-// with 5.5 of 32 lanes active, because in most loop trips SOME lane of the
-// warp admits a node; the 100 list registers also hold the kernel to 22%
-// occupancy.  Serialising the inserting lanes through a warp-cooperative
-// insertion costs the same lane-work (profiles/r02/r02q_coop_list_ab.log:
-// 2x slower), so here each lane keeps the reference's own structure, a
-// bounded max-heap (traverse.hpp:113-175), in shared memory: an admission is
-// a push or a replace-top of <= log2(k) predicated levels (~8 SASS each)
-// instead of k compare-select slots, and the list leaves the registers.
-// Same admission test, same kth bound, so the same visits and the same
-// result set; the slot is written by a heap-sort (extract_sorted).
-// ---------------------------------------------------------------------------
-template <int KB>
-constexpr int smheap_threads() { return KB <= 20 ? 256 : 128; }
-
-template <int KB>
-constexpr size_t smheap_bytes() { return size_t(smheap_threads<KB>()) * KB * sizeof(uint64_t); }
-
-template <int D, int S, int KB>
-__global__ void __launch_bounds__(smheap_threads<KB>()) walk_smheap_kernel(const WalkArgs a) {
-    if (*a.bad != kNoBad) return;  // a rejected batch (batch.cpp:79) writes no slot
-    extern __shared__ uint64_t smheap[];
-    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    LaneWalk<D, S, KB, false, false, true> w;
-    w.hp = smheap + size_t(threadIdx.x >> 5) * 32 * KB + (threadIdx.x & 31);
-    if (i >= a.m || !w.init(a, i)) return;
-    const bool over = a.budget > 0 ? walk_budgeted(w, a, a.budget) : [&] {
-        while (w.step(a)) {
-        }
-        return false;
-    }();
-    w.heap_finish(a, !over);  // over budget: the sorted partial list stays as the later passes' bound
-    if (over) {
-        a.ovf_ids[atomicAdd(a.ovf_count, 1ull)] = uint32_t(w.qi);
-        a.wave_state[w.qi] = make_int2(w.curr, w.prev);  // for the resume pass
     }
 }
 

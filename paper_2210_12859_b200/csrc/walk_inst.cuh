@@ -53,18 +53,6 @@ void launch_one(const WalkArgs& a, cudaStream_t st) {
     launch_walk_grid(walk_kernel<D, S, KB, STATS, UNORDERED>, a, walk_blocks(a.m, kWalkThreads), st);
 }
 
-template <int D, int S, int KB>
-void launch_smheap(const WalkArgs& a, cudaStream_t st) {
-    auto kernel = walk_smheap_kernel<D, S, KB>;
-    constexpr size_t smem = smheap_bytes<KB>();
-    static const bool attr = [&] {
-        cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        return true;
-    }();
-    (void)attr;
-    kernel<<<walk_blocks(a.m, smheap_threads<KB>()), smheap_threads<KB>(), smem, st>>>(a);
-}
-
 template <int D, int S, int KB, bool UNORDERED>
 void launch_round(const WalkArgs& a, cudaStream_t st) {
     launch_walk_grid(walk_round_kernel<D, S, KB, UNORDERED>, a, walk_blocks(a.m, kWalkThreads), st);
@@ -85,12 +73,6 @@ int launch_bucket(const WalkArgs& a, bool stats, bool unordered, int phase, cuda
         else
             launch_round<D, S, KB, false>(a, st);
         return 1;
-    }
-    if constexpr (KB >= 16) {
-        if (a.smheap && !stats && !unordered) {
-            launch_smheap<D, S, KB>(a, st);
-            return 1;
-        }
     }
     if (stats) {
         if (unordered)
