@@ -1396,6 +1396,7 @@ struct DevicePipe {
     std::vector<cudaEvent_t> ev_in;                    // per chunk
     std::vector<cudaEvent_t> ev_sorted, ev_walk, ev_out;  // per job
     cudaEvent_t ev_start = nullptr;                       // FKD_PIPE_TRACE
+    std::vector<cudaEvent_t> ev_wstart, ev_tstart;        // FKD_PIPE_TRACE: walk / tail start per job
     // enqueue thread -> drain thread hand-off
     std::mutex mu;
     std::condition_variable cv;
@@ -1584,6 +1585,10 @@ fkd_status run_host_group(const fkd_tree* t, const float* queries, int64_t m, in
         if (kn.pipe_trace && err == FKD_OK) {
             cudaEventCreate(&P->ev_start);
             cudaEventRecord(P->ev_start, P->wss[0]->cin);
+            P->ev_wstart.assign(P->jobs.size(), nullptr);
+            P->ev_tstart.assign(P->jobs.size(), nullptr);
+            for (auto& e : P->ev_wstart) cudaEventCreate(&e);
+            for (auto& e : P->ev_tstart) cudaEventCreate(&e);
         }
         for (Workspace* w : P->wss) {
             cudaError_t e = reset_small(w, w->stream);
@@ -1692,7 +1697,8 @@ fkd_status run_host_group(const fkd_tree* t, const float* queries, int64_t m, in
                 const bool sharing = b > 0 && share.order != nullptr && use_morton(t, gb.o, jb.count);
                 const fkd_status e =
                     enqueue(t, *P.rep, w, dq, jb.count, gb.o, gb.cap2, dc, dh, nullptr, gb.want_stats, w->stream,
-                            &launches, &wl, kn, nullptr, nullptr, jb.base, w->tail, c == 0 ? kn.first_budget_div : 1,
+                            &launches, &wl, kn, P.ev_start ? P.ev_wstart[j] : nullptr,
+                            P.ev_start ? P.ev_tstart[j] : nullptr, jb.base, w->tail, c == 0 ? kn.first_budget_div : 1,
                             sharing ? &share : nullptr, (b == 0 && B > 1) ? P.ev_sorted[j] : nullptr,
                             io->small + kBatchTotals + 3 * b);
                 if (e != FKD_OK) {
@@ -1822,14 +1828,21 @@ fkd_status run_host_group(const fkd_tree* t, const float* queries, int64_t m, in
             for (int i = 0; i < 3 * B; ++i) tot[size_t(i)] += P->wss[0]->h_small[kBatchTotals + i];
         if (P->ev_start && err == FKD_OK) {  // FKD_PIPE_TRACE: per-job timeline, ms from the first H2D
             for (size_t j = 0; j < P->jobs.size(); ++j) {
-                float tin = 0, tw = 0, tout = 0;
+                float tin = 0, tws = 0, tts = 0, tw = 0, tout = 0;
                 cudaEventElapsedTime(&tin, P->ev_start, P->ev_in[size_t(P->jobs[j].chunk)]);
+                cudaEventElapsedTime(&tws, P->ev_start, P->ev_wstart[j]);
+                cudaEventElapsedTime(&tts, P->ev_start, P->ev_tstart[j]);
                 cudaEventElapsedTime(&tw, P->ev_start, P->ev_walk[j]);
                 cudaEventElapsedTime(&tout, P->ev_start, P->ev_out[j]);
-                std::fprintf(stderr, "dev %d job %zu chunk %d batch %d n=%lld h2d_end %.3f walk_end %.3f d2h_end %.3f\n",
-                             P->di, j, P->jobs[j].chunk, P->jobs[j].b, (long long)P->jobs[j].count, tin, tw, tout);
+                std::fprintf(stderr,
+                             "dev %d job %zu chunk %d batch %d n=%lld h2d_end %.3f walk_start %.3f tail_start %.3f "
+                             "walk_end %.3f d2h_end %.3f\n",
+                             P->di, j, P->jobs[j].chunk, P->jobs[j].b, (long long)P->jobs[j].count, tin, tws, tts, tw,
+                             tout);
             }
             cudaEventDestroy(P->ev_start);
+            for (auto& e : P->ev_wstart) cudaEventDestroy(e);
+            for (auto& e : P->ev_tstart) cudaEventDestroy(e);
         }
         for (Workspace* w : P->wss) release_ws(*P->rep, w);
         for (auto* v : {&P->ev_in, &P->ev_sorted, &P->ev_walk, &P->ev_out})
