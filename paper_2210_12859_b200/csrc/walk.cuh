@@ -280,16 +280,6 @@ __device__ __forceinline__ int dim_down(int d) {  // split dim one level up
 // result lines (kNN8: 76 B per query) displace fewer tree lines in L2.
 // Measured (tools/stream_io_ab.sh, profiles/r01j_stream_io_ab.log): kNN8 walk
 // -0.4% clustered and uniform, fcp +0.3% (so fcp keeps the plain path).
-// Walk-state encodings (A/B knobs): 1-based node ids inside
-// the walk, and prev as two predicates.  Neither changes a visit.
-#ifndef FKD_ONE_BASED
-#define FKD_ONE_BASED 1
-#endif
-#ifndef FKD_PREV_BITS
-#define FKD_PREV_BITS 0
-#endif
-constexpr int32_t kBase = FKD_ONE_BASED ? 1 : 0;  // walk id of node 0
-
 #ifndef FKD_STREAM_QUERY_LOADS
 #define FKD_STREAM_QUERY_LOADS 1
 #endif
@@ -315,17 +305,7 @@ struct LaneWalk {
     float q[D];
     float qr[kRot ? D : 1];
     uint64_t L[kSlot ? 1 : KB];  // slot mode: L[0] is the kth key
-    // curr: the node (1-based with FKD_ONE_BASED: children 2c / 2c+1, parent
-    // c >> 1, one instruction each); with FKD_PREV_BITS the reference's prev
-    // is carried as two predicates — whether the walk arrived from the parent
-    // and, if it came up, whether from the right child — which is all that
-    // traverse_step reads of it (traverse.hpp:216, 232-238).
-    int32_t curr;
-#if FKD_PREV_BITS
-    bool down_in, up_right;
-#else
-    int32_t prev;
-#endif
+    int32_t curr, prev;  // 1-based node ids (the reference's + 1)
     int d;  // split dim of curr, tracked incrementally (tree.hpp:27-29)
     float r2;
     int64_t qi;
@@ -366,49 +346,20 @@ struct LaneWalk {
 #pragma unroll
             for (int j = 0; j < KB; ++j) L[j] = j < dummies ? 0ull : empty;
         }
-        curr = kBase;  // the root, entered from its parent -1 (traverse.hpp:252)
-#if FKD_PREV_BITS
-        down_in = true;
-        up_right = false;
-#else
-        prev = kBase - 1;
-#endif
+        curr = 1;  // 1-based ids inside the walk: the root, entered from its parent 0 (= -1)
+        prev = 0;
         d = 0;
         r2 = a.cap2;
         cnt = Counters<STATS>();
         return true;
     }
 
-    // 0-based ids of the reference's (curr, prev), for parking a walk
-    __device__ __forceinline__ int32_t node() const { return curr - kBase; }
-    __device__ __forceinline__ int32_t prev_node() const {
-#if FKD_PREV_BITS
-        const int32_t c = curr - kBase;
-        return down_in ? ((c - 1) >> 1) : 2 * c + (up_right ? 2 : 1);
-#else
-        return prev - kBase;
-#endif
-    }
-    __device__ __forceinline__ void set_state(int32_t c0, int32_t p0) {  // 0-based (curr, prev)
-        curr = c0 + kBase;
-#if FKD_PREV_BITS
-        down_in = p0 < c0;
-        up_right = (p0 & 1) == 0;  // a right child 2c+2 is even
-#else
-        prev = p0 + kBase;
-#endif
-    }
-
     // One transition of traverse_step (traverse.hpp:198-248) plus the
     // in-register bounces.  Returns false once the root stepped to -1.
     __device__ __forceinline__ bool step(const WalkArgs& a) {
-        const int32_t n = a.n + kBase;  // ids < n exist
-#if FKD_PREV_BITS
-        const bool from_parent = down_in;
-#else
+        const int32_t n = a.n;  // 1-based ids: node c exists iff c <= n
         const bool from_parent = prev < curr;
-#endif
-        const float* nodes = a.nodes - kBase * S;  // nodes[curr] is the node's slot
+        const float* nodes = a.nodes - S;  // nodes + c * S is 1-based node c's slot
         float p[D];
         float pd;
         if constexpr (S == D && D > 1) {
@@ -437,7 +388,7 @@ struct LaneWalk {
             // 2-D fcp walk would take 44 instead of 28 registers),
             // admission is predicated on a first visit.
             const float d2 = sq_dist<D, (D <= 4 && KB <= 8)>(q, p);
-            const uint64_t key = make_key(d2, curr - kBase);
+            const uint64_t key = make_key(d2, curr - 1);
             if constexpr (kSlot) {
                 if (from_parent && key_lt(key, L[0])) {
                     slot_insert(a, key);
@@ -449,7 +400,7 @@ struct LaneWalk {
             }
         } else if (from_parent) {  // fcp, D != 3: a branch is cheaper than the FP ops
             const float d2 = sq_dist<D, (D <= 4 && KB <= 8)>(q, p);
-            const uint64_t key = make_key(d2, curr - kBase);
+            const uint64_t key = make_key(d2, curr - 1);
             if constexpr (kSlot) {
                 if (key_lt(key, L[0])) {
                     slot_insert(a, key);
@@ -470,13 +421,10 @@ struct LaneWalk {
         const float sd = __fsub_rn(qd, pd);                         // 226
         const bool cs = sd > 0.0f;                                 // 227
         const bool fir = __fmul_rn(sd, sd) <= r2;                  // 230
-#if FKD_ONE_BASED
-        const int32_t parent = curr >> 1;                          // 205 (1-based): root -> 0 = "-1"
+        // 205, 228-229 with 1-based ids (c = node + 1): parent c >> 1 (the
+        // root's is 0, i.e. -1), children 2c and 2c + 1 — one instruction each
+        const int32_t parent = curr >> 1;
         const int32_t l = curr << 1, r = l | 1;
-#else
-        const int32_t parent = (curr - 1) >> 1;                    // 205: (c+1)/2-1, root -> -1
-        const int32_t l = 2 * curr + 1, r = l + 1;
-#endif
         int32_t next;
         bool down;
         if constexpr (!UNORDERED) {
@@ -486,15 +434,10 @@ struct LaneWalk {
             // from the parent, an empty close slot bounces straight back,
             // which is a return from the close child; an empty far slot
             // bounces back, which is a return from the far child (-> parent).
-            const bool close_ok = close < n;
+            const bool close_ok = close <= n;
             const bool go_close = from_parent && close_ok;
-#if FKD_PREV_BITS
-            const bool came_from_close = up_right == cs;           // close = cs ? r : l
-#else
-            const bool came_from_close = prev == close;
-#endif
-            const bool try_far = from_parent ? !close_ok : came_from_close;
-            const bool far_ok = far < n;
+            const bool try_far = from_parent ? !close_ok : prev == close;
+            const bool far_ok = far <= n;
             const bool go_far = try_far && fir && far_ok;
             if constexpr (STATS) {
                 if (from_parent && !close_ok) cnt.step(2, 1, 0);
@@ -509,22 +452,18 @@ struct LaneWalk {
             if (from_parent)
                 next = enter_left ? l : (enter_right ? r : parent);
             else
-#if FKD_PREV_BITS
-                next = (!up_right && enter_right) ? r : parent;
-#else
                 next = (prev == l && enter_right) ? r : parent;
-#endif
-            if (next >= n) {
+            if (next > n) {
                 cnt.step(2, 1, 0);
                 next = (next == l && enter_right) ? r : parent;
-                if (next >= n) {
+                if (next > n) {
                     cnt.step(2, 1, 0);
                     next = parent;
                 }
             }
             down = next != parent;
         }
-        if (!down && curr == kBase) return false;  // 240-244: the root stepped to -1
+        if (!down && curr == 1) return false;  // 240-244: the root stepped to -1
         if constexpr (kRot) {
             float t[D];
 #pragma unroll
@@ -534,12 +473,7 @@ struct LaneWalk {
         } else {
             d = down ? dim_up<D>(d) : dim_down<D>(d);
         }
-#if FKD_PREV_BITS
-        down_in = down;
-        up_right = (curr & 1) == (FKD_ONE_BASED ? 1 : 0);  // leaving a right child (1-based odd, 0-based even)
-#else
         prev = curr;
-#endif
         curr = next;
         return true;
     }
@@ -593,8 +527,9 @@ struct LaneWalk {
             }
         }
         r2 = key_dist(L[kSlot ? 0 : KB - 1]);
-        const int2 st = a.wave_state[qi];
-        set_state(st.x, st.y);
+        const int2 st = a.wave_state[qi];  // 0-based (curr, prev)
+        curr = st.x + 1;
+        prev = st.y + 1;
         d = depth_of(st.x) % D;
         if constexpr (kRot) {
             // qr[j] = q[(d + j) % D] as d predicated one-place rotations: a
@@ -782,7 +717,7 @@ __global__ void __launch_bounds__(kWalkThreads, walk_min_blocks<D, KB>()) walk_k
         w.finish(a, !over);  // over budget: the partial list stays as the overflow pass's bound
         if (over) {
             a.ovf_ids[atomicAdd(a.ovf_count, 1ull)] = uint32_t(w.qi);
-            a.wave_state[w.qi] = make_int2(w.node(), w.prev_node());  // for the resume pass
+            a.wave_state[w.qi] = make_int2(w.curr - 1, w.prev - 1);  // 0-based, for the resume pass
         }
     }
     if (active) add_totals<STATS>(a, w.cnt.steps, w.cnt.visited, w.cnt.processed);
@@ -815,7 +750,7 @@ __global__ void __launch_bounds__(kWalkThreads, walk_min_blocks<D, KB>()) walk_r
         w.resume(a, int32_t(qid));
         park = walk_budgeted(w, a, a.trips);
         w.finish(a, !park);
-        if (park) a.wave_state[qid] = make_int2(w.node(), w.prev_node());
+        if (park) a.wave_state[qid] = make_int2(w.curr - 1, w.prev - 1);
     }
     const unsigned lane = threadIdx.x & 31u;
     const unsigned mask = __ballot_sync(0xffffffffu, park);
