@@ -1001,7 +1001,13 @@ fkd_status fkd_tree_add_replicas(fkd_tree* t, const int32_t* devices, int32_t nd
         return fail(FKD_NO_DEVICE, "no CUDA device visible (the B200 path has no CPU fallback)");
     for (int32_t i = 0; i < ndev; ++i)
         if (devices[i] < 0 || devices[i] >= count) return fail(FKD_INVALID_ARGUMENT, "device id out of range");
-    return fanout_replicas(t, std::vector<int>(devices, devices + ndev));
+    const size_t had = t->reps.size();
+    const fkd_status s = fanout_replicas(t, std::vector<int>(devices, devices + ndev));
+    if (s != FKD_OK) {  // a failed fan-out leaves the tree as it was (no half-copied replica)
+        for (size_t i = had; i < t->reps.size(); ++i) delete t->reps[i];
+        t->reps.resize(had);
+    }
+    return s;
 }
 
 fkd_status fkd_tree_create_device(const float* d_level_order, int64_t n, int32_t dim, void* stream,
