@@ -54,14 +54,21 @@ int walk_bucket_of(int k);
 // The rounds run for register lists of <= 4 slots (fcp, k <= 4) and, in
 // batches of >= 2^22 queries, 8 slots (a 1M-query kNN8 batch is 4-8% slower
 // with them: the round boundaries cost more than the small batch's warps lose).
-inline bool rounds_on(int k, int64_t m, const Knobs& kn) {
+// From 7-D up walks are thousands of trips long (8-D kNN16: ~6k with box
+// pruning): kNN lists take no rounds and a first budget of 8192 trips, fcp
+// 1024 (8-D, M = 1M: kNN16 123 -> 101 ms, kNN8 85 -> 73, fcp 33.6 -> 28.2;
+// 5-D / 6-D indifferent; profiles/r02/r02ad_budget_hd.log).
+constexpr int kLongWalkDim = 7;
+inline bool rounds_on(int k, int64_t m, const Knobs& kn, int dim) {
     const int kb = walk_bucket_of(k);
+    if (dim >= kLongWalkDim && k > 1) return false;
     return kb <= 4 || (kb == 8 && m >= kn.rounds_min_m);
 }
 // first walk's loop trips before a query parks (FKD_BUDGET < 0: per kind)
-inline int first_budget(int k, int64_t m, const Knobs& kn) {
+inline int first_budget(int k, int64_t m, const Knobs& kn, int dim) {
+    if (dim >= kLongWalkDim) return k == 1 ? 1024 : 8192;
     if (k == 1) return 112;
-    if (!rounds_on(k, m, kn)) return 3072;
+    if (!rounds_on(k, m, kn, dim)) return 3072;
     return walk_bucket_of(k) <= 4 ? 256 : 384;
 }
 // resume pass trips (FKD_RESUME_TRIPS = 0): 4 x the per-kind budget without rounds
@@ -78,11 +85,11 @@ inline int resume_trips_default(int k) { return k == 1 ? 4096 : 49152; }
 // the CTA pass than in a latency-bound 448-trip round (clustered 1.25M / 2.5M:
 // -22% / -13%), while at 10M the third round keeps the resume pass off (C3 fcp
 // 2.49 vs 3.03 ms without it; profiles/r01i_fcp_*ab.log).
-const std::vector<int>& round_schedule(const Knobs& kn, int k, int64_t m) {
+const std::vector<int>& round_schedule(const Knobs& kn, int k, int64_t m, int dim) {
     static const std::vector<int> none;
     if (k == 1) return (kn.rounds_fcp_env || m >= kn.rounds_min_m) ? kn.rounds_fcp : kn.rounds_fcp_small;
     if (kn.rounds_knn_all) return kn.rounds_knn_env;
-    if (!rounds_on(k, m, kn)) return none;
+    if (!rounds_on(k, m, kn, dim)) return none;
     return walk_bucket_of(k) <= 4 ? kn.rounds_knn4 : kn.rounds_knn8;
 }
 
@@ -609,7 +616,7 @@ fkd_status enqueue(const fkd_tree* t, Replica& r, Workspace* w, const float* d_q
         a.per_query = d_per_query ? d_per_query + base : nullptr;
         a.bad = w->small;
         a.id_base = id_offset + base;
-        int budget = tu.budget >= 0 ? tu.budget : first_budget(k, cm, tu);
+        int budget = tu.budget >= 0 ? tu.budget : first_budget(k, cm, tu, t->dim);
         if (budget_div > 1 && budget > 0) budget = std::max(64, budget / budget_div);
         a.budget = (stats || walk_bucket_of(k) == 0 || t->dim > 8) ? 0 : budget;
         if (a.budget > 0) {
@@ -655,7 +662,7 @@ fkd_status enqueue(const fkd_tree* t, Replica& r, Workspace* w, const float* d_q
                 FKD_CUDA(cudaStreamWaitEvent(tail_st, w->pe[3], 0));
             }
             const cudaStream_t ts = (a.budget > 0 && tail_st) ? tail_st : st;
-            const std::vector<int>& rounds = round_schedule(tu, k, cm);
+            const std::vector<int>& rounds = round_schedule(tu, k, cm, t->dim);
             if (a.budget > 0 && !rounds.empty()) {
                 // continuation rounds: the parked walks, compacted into dense
                 // warps, continue for `trips` more trips per round; lists

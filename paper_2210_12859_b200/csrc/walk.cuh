@@ -287,8 +287,36 @@ __device__ __forceinline__ int dim_down(int d) {  // split dim one level up
 #define FKD_STREAM_IO_MIN_KB 8
 #endif
 
+// Box pruning (incremental distance, Arya & Mount): from this dimension up,
+// the production walk (not STATS, not unordered) enters a far child only if
+// the squared distance from the query to the far child's whole cell is within
+// radius2, instead of the split plane alone (traverse.hpp:230).  The cell's
+// per-dimension offsets come from the deepest ancestor in that dimension
+// whose path went to its far side; their squares are summed left to right
+// with the same round-to-nearest ops as the point distance, term by term no
+// larger than any point of the cell's, so the test never prunes a node the
+// reference would admit: same result set, same bits, fewer nodes (oracle
+// simulation, N = 1M uniform: 8-D kNN16 12.3k -> 3.1k processed per query,
+// 4-D kNN50 794 -> 508, 3-D kNN8 107 -> 91).  STATS mode keeps the
+// reference's plane test, so the counters stay the reference's.  Measured
+// (N = 10M uniform, profiles/r02/r02ac_box_pruning_ab.log): 8-D kNN16
+// 270 -> 123 ms, 6-D kNN8 23.4 -> 13.7, 5-D kNN16 14.3 -> 10.5; in 4-D the
+// offsets' registers and instructions cost more than the pruning saves (kNN8
+// +16%, kNN50 +40% at 138 registers), so the mode starts at 5-D.
+#ifndef FKD_BOX_MIN_D
+#define FKD_BOX_MIN_D 5
+#endif
+
+template <int D>
+constexpr uint32_t dim_levels_mask() {  // bits 0, D, 2D, ... below 32
+    uint32_t m = 0;
+    for (int i = 0; i < 32; i += D) m |= 1u << i;
+    return m;
+}
+
 template <int D, int S, int KB, bool STATS, bool UNORDERED>
 struct LaneWalk {
+    static constexpr bool kBox = D >= FKD_BOX_MIN_D && D > 1 && !STATS && !UNORDERED;
     // With a split-plane slot in the store (S > D) the walk never needs the
     // split dimension: qr holds the query rotated so that qr[0] is the
     // coordinate split at the current depth (rotated by one per level).
@@ -307,6 +335,10 @@ struct LaneWalk {
     uint64_t L[kSlot ? 1 : KB];  // slot mode: L[0] is the kth key
     int32_t curr, prev;  // 1-based node ids (the reference's + 1)
     int d;  // split dim of curr, tracked incrementally (tree.hpp:27-29)
+    // box mode: squared per-dimension offsets of curr's cell from the query,
+    // and bit l set iff the path from level l went to the far child
+    float osq[kBox ? D : 1];
+    uint32_t farmask;
     float r2;
     int64_t qi;
     Counters<STATS> cnt;
@@ -349,6 +381,11 @@ struct LaneWalk {
         curr = 1;  // 1-based ids inside the walk: the root, entered from its parent 0 (= -1)
         prev = 0;
         d = 0;
+        if constexpr (kBox) {
+#pragma unroll
+            for (int j = 0; j < D; ++j) osq[j] = 0.0f;
+            farmask = 0;
+        }
         r2 = a.cap2;
         cnt = Counters<STATS>();
         return true;
@@ -420,13 +457,27 @@ struct LaneWalk {
             qd = pick(q, d);
         const float sd = __fsub_rn(qd, pd);                         // 226
         const bool cs = sd > 0.0f;                                 // 227
-        const bool fir = __fmul_rn(sd, sd) <= r2;                  // 230
+        const float sd2 = __fmul_rn(sd, sd);
+        bool fir;
+        if constexpr (kBox) {
+            // the far child's cell: this cell with offset |sd| in the split dim
+            float box = 0.0f;
+#pragma unroll
+            for (int i = 0; i < D; ++i) {
+                const float t = (i == d) ? sd2 : osq[i];
+                box = i == 0 ? t : __fadd_rn(box, t);
+            }
+            fir = box <= r2;
+        } else {
+            fir = sd2 <= r2;                                       // 230
+        }
         // 205, 228-229 with 1-based ids (c = node + 1): parent c >> 1 (the
         // root's is 0, i.e. -1), children 2c and 2c + 1 — one instruction each
         const int32_t parent = curr >> 1;
         const int32_t l = curr << 1, r = l | 1;
         int32_t next;
         bool down;
+        bool to_far = false, back_far = false;  // box mode: entering / leaving the far child
         if constexpr (!UNORDERED) {
             const int32_t close = cs ? r : l;                      // 228
             const int32_t far = cs ? l : r;                        // 229
@@ -445,6 +496,8 @@ struct LaneWalk {
             }
             down = go_close || go_far;
             next = go_close ? close : (go_far ? far : parent);
+            to_far = go_far;
+            back_far = !from_parent && prev != close;
         } else {
             // left-first order; a child is entered iff it is on the query's
             // side or its plane is within the radius
@@ -464,18 +517,72 @@ struct LaneWalk {
             down = next != parent;
         }
         if (!down && curr == 1) return false;  // 240-244: the root stepped to -1
+        if constexpr (kBox) box_update(a, down, to_far, sd2, back_far);
         if constexpr (kRot) {
             float t[D];
 #pragma unroll
             for (int j = 0; j < D; ++j) t[j] = down ? qr[(j + 1) % D] : qr[(j + D - 1) % D];
 #pragma unroll
             for (int j = 0; j < D; ++j) qr[j] = t[j];
+            if constexpr (kBox) d = down ? dim_up<D>(d) : dim_down<D>(d);
         } else {
             d = down ? dim_up<D>(d) : dim_down<D>(d);
         }
         prev = curr;
         curr = next;
         return true;
+    }
+
+    // The split coordinate of (1-based) node c, split in dim dim.
+    __device__ __forceinline__ float plane_of(const WalkArgs& a, int32_t c, int dim) const {
+        const float* base = a.nodes + size_t(c - 1) * S;
+        if constexpr (S > D && D > 1) return __ldg(base + (S - 1));  // the padding slot holds it
+        else return __ldg(base + dim);
+    }
+    // Box mode, after a transition out of curr (split dim d): entering a
+    // child records the decision bit of this level (and, for the far child,
+    // its offset); leaving curr upward after its far child restores curr's
+    // own offset in d, from the deepest same-dimension ancestor whose path
+    // went far (one load; 0 if none).
+    __device__ __forceinline__ void box_update(const WalkArgs& a, bool down, bool to_far, float sd2, bool back_from_far) {
+        const int lvl = 31 - __clz(curr);
+        if (down) {
+            farmask = to_far ? (farmask | (1u << lvl)) : (farmask & ~(1u << lvl));
+            if (to_far) {
+#pragma unroll
+                for (int i = 0; i < D; ++i) osq[i] = (i == d) ? sd2 : osq[i];
+            }
+        } else if (back_from_far) {
+            const uint32_t cand = farmask & (dim_levels_mask<D>() << d) & ((1u << lvl) - 1u);
+            float o2 = 0.0f;
+            if (cand) {
+                const int la = 31 - __clz(cand);
+                const float o = __fsub_rn(pick(q, d), plane_of(a, curr >> (lvl - la), d));
+                o2 = __fmul_rn(o, o);
+            }
+#pragma unroll
+            for (int i = 0; i < D; ++i) osq[i] = (i == d) ? o2 : osq[i];
+        }
+    }
+    // Box mode, resuming a parked walk: the path's decisions and offsets from
+    // the root down to curr (one load per level).
+    __device__ __forceinline__ void box_recompute(const WalkArgs& a) {
+#pragma unroll
+        for (int j = 0; j < D; ++j) osq[j] = 0.0f;
+        farmask = 0;
+        const int L = 31 - __clz(curr);
+        for (int lv = 0; lv < L; ++lv) {
+            const int32_t anc = curr >> (L - lv), child = curr >> (L - lv - 1);
+            const int da = lv % D;
+            const float sda = __fsub_rn(pick(q, da), plane_of(a, anc, da));
+            const bool close_right = sda > 0.0f;
+            if (((child & 1) != 0) != close_right) {  // went to the far child
+                farmask |= 1u << lv;
+                const float o2 = __fmul_rn(sda, sda);
+#pragma unroll
+                for (int i = 0; i < D; ++i) osq[i] = (i == da) ? o2 : osq[i];
+            }
+        }
     }
 
     // Sorted insertion into the output slot (slot mode): x passes the
@@ -531,6 +638,7 @@ struct LaneWalk {
         curr = st.x + 1;
         prev = st.y + 1;
         d = depth_of(st.x) % D;
+        if constexpr (kBox) box_recompute(a);
         if constexpr (kRot) {
             // qr[j] = q[(d + j) % D] as d predicated one-place rotations: a
             // select chain on d is folded back into a dynamic index by the
@@ -641,7 +749,7 @@ __device__ __forceinline__ void add_totals(const WalkArgs& a, unsigned long long
 // (+0.5%) and 2-D/3-D/4-D (+0.4-0.8%) lose that way (tools/occ16_ab.sh,
 // tools/occ16_hd_ab.sh, profiles/r01i_occ16_*ab.log)
 #ifndef FKD_MINB_KB16_HIGH_D
-#define FKD_MINB_KB16_HIGH_D 4
+#define FKD_MINB_KB16_HIGH_D 1  // round 1: 4 (-3.5% in 5-D); with box pruning (r02) 1 is 2% better
 #endif
 // 16-slot walks whose list lives in the output slot (LaneWalk::kSlot, 8-D):
 // 5 blocks (48 registers, 40 B of spill stores) -> 8-D kNN16 walk 300 -> 281 ms;
