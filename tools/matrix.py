@@ -81,7 +81,9 @@ def run(ref, name, n, m, dim, data, batches, cpu_sample, unordered=(False,), rep
                    "tail_ms": float(np.median(tail)), "walk_qps": mm / w * 1e3,
                    "batch_qps": mm / (w + o) * 1e3, "P_bar": p, "steps_per_query": st.steps / mm,
                    "bytes_per_query": bq(dim, p, stride),
-                   "hbm_frac": mm * bq(dim, p, stride) / (w * 1e-3) / 1e9 / HBM}
+                   "hbm_frac": mm * bq(dim, p, stride) / (w * 1e-3) / 1e9 / HBM,
+                   "note": ("P_bar is the reference walk's (STATS pass); from 5-D the production walk "
+                            "prunes by cell box and processes fewer nodes") if dim >= 5 else ""}
             if cpu_sample and not uo:
                 s = min(m, cpu_sample)
                 qsam = np.ascontiguousarray(qs[:s])
