@@ -848,3 +848,51 @@ def test_morton_keys_and_exchange_single_rank(oracle):
     bad[17, 1] = float("nan")
     with pytest.raises(fk.DataError, match="point 17"):
         fk.morton_keys(tree, bad)
+
+
+def test_concurrent_grouped_and_device_submissions(oracle):
+    """Several host threads at once through the grouped host pipeline
+    (pageable buffers: staging rings + drain threads) and the concurrent
+    device submission, sharing one tree with two replicas: every result equals
+    the single-caller answer (pooled workspaces, staging pool, copy pool and
+    per-device threads under contention)."""
+    import threading
+
+    import torch
+
+    nodes = oracle.build_tree(oracle.random_points(81, 60_000, 3))
+    tree = fk.KdTree.from_level_order(nodes, devices=[0, 0])
+    work = []
+    for t in range(6):
+        qs = fk.clustered_points(82 + t, 2, 300_000 + 7919 * t, 3)
+        specs = [(qs, fk.BatchOptions(kind=fk.QueryKind.knn, k=8)), (qs, fk.BatchOptions()),
+                 (qs, fk.BatchOptions(kind=fk.QueryKind.knn, k=3, max_radius=0.05))]
+        work.append((qs, specs, [fk.run_batch(tree, q, o) for q, o in specs]))
+    errors = []
+
+    def worker(i):
+        qs, specs, refs = work[i]
+        try:
+            for rep in range(3):
+                if (i + rep) % 2 == 0:
+                    got = fk.run_batches(tree, specs)
+                    for g, r in zip(got, refs):
+                        assert np.array_equal(g.counts, r.counts) and g.hits.tobytes() == r.hits.tobytes()
+                else:
+                    dq = torch.from_numpy(qs).cuda()
+                    outs = [(torch.empty(len(qs), dtype=torch.int32, device="cuda"),
+                             torch.empty(len(qs) * o.stride, dtype=torch.int64, device="cuda")) for _, o in specs]
+                    stream = torch.cuda.Stream()
+                    fk.run_batches_device(tree, [(dq, c, h, o) for (c, h), (_, o) in zip(outs, specs)], stream=stream)
+                    for (c, h), r in zip(outs, refs):
+                        assert np.array_equal(c.cpu().numpy(), r.counts)
+                        assert h.cpu().numpy().tobytes() == r.hits.tobytes()
+        except Exception as e:  # noqa: BLE001
+            errors.append((i, repr(e)))
+
+    threads = [threading.Thread(target=worker, args=(i,)) for i in range(6)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    assert not errors, errors
