@@ -265,6 +265,13 @@ fkd_status fkd_clustered_points(uint64_t master_seed, uint64_t stream, int64_t c
 void* fkd_host_alloc(size_t bytes);
 void fkd_host_free(void* p);
 
+/* Profiling builds (-DFKD_BLOCK_TRACE=1) only: every walk / round / CTA-pass
+ * block appends {tag, SM id, start ns, end ns} (%globaltimer; tag = list
+ * length << 8 | phase) to d_records (device, cap records of 24 bytes; the
+ * device counter d_counter must start at 0).  NULL disables.  Other builds
+ * return FKD_INVALID_ARGUMENT for a non-NULL buffer. */
+fkd_status fkd_debug_block_trace(void* d_records, void* d_counter, int64_t cap);
+
 /* Thread-local message for the last non-OK status. */
 const char* fkd_last_error(void);
 

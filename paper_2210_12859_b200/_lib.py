@@ -15,7 +15,7 @@ EXPORTS = (
     "fkd_default_options", "fkd_tree_create", "fkd_tree_create_device", "fkd_tree_destroy",
     "fkd_tree_size", "fkd_tree_dim", "fkd_tree_replicas", "fkd_tree_add_replicas", "fkd_morton_keys", "fkd_run_batch", "fkd_run_batches", "fkd_run_batch_device", "fkd_run_batches_device", "fkd_fcp", "fkd_knn",
     "fkd_build_tree", "fkd_build_tree_device", "fkd_tree_build", "fkd_result_hash", "fkd_random_points", "fkd_clustered_points",
-    "fkd_host_alloc", "fkd_host_free", "fkd_last_error", "fkd_version", "fkd_trace_batch",
+    "fkd_host_alloc", "fkd_host_free", "fkd_debug_block_trace", "fkd_last_error", "fkd_version", "fkd_trace_batch",
     "fkd_file_info", "fkd_read_file_device", "fkd_write_file", "fkd_tree_load",
 )
 
@@ -85,6 +85,7 @@ def _load() -> C.CDLL:
     lib.fkd_read_file_device.argtypes = [C.c_char_p, i32, vp, i64, vp, vp, vp]
     lib.fkd_write_file.argtypes = [C.c_char_p, i32, vp, i64, i32]
     lib.fkd_tree_load.argtypes = [C.c_char_p, vp, i32, vp]
+    lib.fkd_debug_block_trace.argtypes = [vp, vp, i64]
     lib.fkd_host_alloc.restype = vp
     lib.fkd_host_alloc.argtypes = [C.c_size_t]
     lib.fkd_host_free.argtypes = [vp]

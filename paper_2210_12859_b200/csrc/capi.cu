@@ -46,6 +46,14 @@ fkd_status fail(fkd_status s, const std::string& msg) {
     } while (0)
 
 constexpr int64_t kSortChunk = int64_t(1) << 30;  // u32 ids, int item counts in CUB
+// Block timeline buffer (fkd_debug_block_trace; FKD_BLOCK_TRACE builds only)
+struct BlockTraceConfig {
+    BlockTraceRec* buf = nullptr;
+    unsigned long long* next = nullptr;
+    long long cap = 0;
+};
+BlockTraceConfig g_btrace;
+
 constexpr int kSmallWords = 64;   // per-workspace device counters (Workspace::small)
 constexpr int kBatchTotals = 16;  // first per-batch totals word
 constexpr int kMaxGroup = (kSmallWords - kBatchTotals) / 3;  // batches per host pipeline
@@ -602,6 +610,10 @@ fkd_status enqueue(const fkd_tree* t, Replica& r, Workspace* w, const float* d_q
         const int64_t cm = std::min(chunk, m - base);
         WalkArgs a{};
         a.nodes = r.nodes;
+        a.btrace = g_btrace.buf;  // tag: the list length (fcp 1) and the kernel phase
+        a.btrace_next = g_btrace.next;
+        a.btrace_cap = g_btrace.cap;
+        a.btrace_tag = uint32_t(k) << 8;
         a.n = int32_t(t->n);
         a.dim = t->dim;
         a.stride = t->stride;
@@ -794,6 +806,15 @@ fkd_status fkd_morton_keys(const fkd_tree* t, const float* d_queries, int64_t m,
     FKD_CUDA(cudaFreeAsync(bad, st));
     FKD_CUDA(cudaStreamSynchronize(st));
     if (h != kNoBad) return fail(FKD_DATA_ERROR, "queries: non-finite coordinate in point " + std::to_string(h));
+    return FKD_OK;
+}
+
+fkd_status fkd_debug_block_trace(void* d_records, void* d_counter, int64_t cap) {
+    if (d_records && !FKD_BLOCK_TRACE)
+        return fail(FKD_INVALID_ARGUMENT, "library built without FKD_BLOCK_TRACE (make EXTRA=-DFKD_BLOCK_TRACE=1)");
+    g_btrace.buf = static_cast<BlockTraceRec*>(d_records);
+    g_btrace.next = static_cast<unsigned long long*>(d_counter);
+    g_btrace.cap = d_records ? cap : 0;
     return FKD_OK;
 }
 

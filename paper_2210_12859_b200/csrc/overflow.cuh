@@ -79,11 +79,17 @@ __global__ void __launch_bounds__(THREADS) overflow_kernel(const WalkArgs a) {
     const bool resumed = a.resume_min > 0 && *a.ovf_count >= (unsigned long long)a.resume_min;
     const uint32_t* ids = resumed ? a.wave_out : a.ovf_ids;
     const unsigned long long count = resumed ? *a.wave_n_out : *a.ovf_count;
+    BlockTrace bt(a);
+    bool worked = false;
     while (true) {
         if (tid == 0) slot = atomicAdd(a.ovf_next, 1ull);
         __syncthreads();
         const unsigned long long s = slot;
-        if (s >= count) return;
+        if (s >= count) {
+            if (worked) bt.end(a, 1);
+            return;
+        }
+        worked = true;
         const int64_t qi = ids[s];
 
         float q[D];

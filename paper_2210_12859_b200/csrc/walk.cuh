@@ -40,6 +40,18 @@ namespace fkd {
 constexpr uint64_t kEmptyKey = (uint64_t(0x7f800000u + 1u) << 32) | 0xFFFFFFFFull;
 constexpr uint64_t kNoBad = ~0ull;
 
+// Block timeline instrumentation (profiling builds only: -DFKD_BLOCK_TRACE=1;
+// tools/sm_timeline.py).  Each traced block appends {tag, SM, start, end}
+// (%globaltimer ns) so the SM occupancy of a whole step — concurrent batches
+// included — can be reconstructed without a profiler serialising kernels.
+#ifndef FKD_BLOCK_TRACE
+#define FKD_BLOCK_TRACE 0
+#endif
+struct BlockTraceRec {
+    uint32_t tag, smid;
+    unsigned long long t0, t1;
+};
+
 struct WalkArgs {
     const float* nodes;         // device tree store, `stride` floats per node
     int32_t n;                  // tree size
@@ -70,6 +82,38 @@ struct WalkArgs {
     int2* wave_state;                      // [m] (curr, prev) of suspended walks
     int64_t resume_min;                    // >= this many over-budget queries: resume them with
                                            // the plain grid instead of the CTA overflow pass
+    BlockTraceRec* btrace;                 // FKD_BLOCK_TRACE builds: record buffer (null: off)
+    unsigned long long* btrace_next;
+    long long btrace_cap;
+    uint32_t btrace_tag;                   // batch id << 8 | kernel phase
+};
+
+__device__ __forceinline__ unsigned long long trace_clock() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Call at block start (all threads); end() where every thread of the block
+// arrives together.  Compiles to nothing without FKD_BLOCK_TRACE.
+struct BlockTrace {
+    unsigned long long t0 = 0;
+    __device__ __forceinline__ explicit BlockTrace(const WalkArgs& a) {
+        if constexpr (FKD_BLOCK_TRACE) {
+            if (a.btrace && threadIdx.x == 0) t0 = trace_clock();
+        }
+    }
+    __device__ __forceinline__ void end(const WalkArgs& a, uint32_t phase) {
+        if constexpr (FKD_BLOCK_TRACE) {
+            __syncthreads();
+            if (a.btrace && threadIdx.x == 0) {
+                const unsigned long long i = atomicAdd(a.btrace_next, 1ull);
+                unsigned sm;
+                asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+                if (i < (unsigned long long)a.btrace_cap) a.btrace[i] = BlockTraceRec{a.btrace_tag | phase, sm, t0, trace_clock()};
+            }
+        }
+    }
 };
 
 __device__ __forceinline__ uint64_t make_key(float d2, int32_t node) {
@@ -806,6 +850,7 @@ __device__ __forceinline__ bool walk_budgeted(W& w, const WalkArgs& a, int trips
 template <int D, int S, int KB, bool STATS, bool UNORDERED>
 __global__ void __launch_bounds__(kWalkThreads, walk_min_blocks<D, KB>()) walk_kernel(const WalkArgs a) {
     if (*a.bad != kNoBad) return;  // a rejected batch (batch.cpp:79) writes no slot
+    BlockTrace bt(a);
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     LaneWalk<D, S, KB, STATS, UNORDERED> w;
     bool active = i < a.m && w.init(a, i);
@@ -830,6 +875,7 @@ __global__ void __launch_bounds__(kWalkThreads, walk_min_blocks<D, KB>()) walk_k
     }
     if (active) add_totals<STATS>(a, w.cnt.steps, w.cnt.visited, w.cnt.processed);
     else add_totals<STATS>(a, 0, 0, 0);
+    bt.end(a, 0);
 }
 
 // Continuation round (compaction rounds): one thread per id
@@ -849,6 +895,7 @@ __global__ void __launch_bounds__(kWalkThreads, walk_min_blocks<D, KB>()) walk_r
     if (a.resume_min > 0 && items < a.resume_min) return;
     const int64_t first = int64_t(blockIdx.x) * blockDim.x;
     if (first >= items) return;
+    BlockTrace bt(a);
     const int64_t i = first + threadIdx.x;
     bool park = false;
     uint32_t qid = 0;
@@ -869,6 +916,7 @@ __global__ void __launch_bounds__(kWalkThreads, walk_min_blocks<D, KB>()) walk_r
         base = __shfl_sync(0xffffffffu, base, leader);
         if (park) a.wave_out[base + __popc(mask & ((1u << lane) - 1u))] = qid;
     }
+    bt.end(a, 3);
 }
 
 // ---------------------------------------------------------------------------
