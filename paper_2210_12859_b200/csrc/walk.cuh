@@ -378,6 +378,11 @@ struct LaneWalk {
     float qr[kRot ? D : 1];
     uint64_t L[kSlot ? 1 : KB];  // slot mode: L[0] is the kth key
     int32_t curr, prev;  // 1-based node ids (the reference's + 1)
+    // D <= 3: from_parent carried from the last transition and the children
+    // formed by bit ops — ~1.5% faster 3-D walks, but 3-8% slower 4-D ones
+    // (same-box A/B, profiles/r02/r02ah_transition_forms_ab.log), so only there
+    static constexpr bool kCarry = D <= 3;
+    bool fromp;  // kCarry: arrived from the parent (prev < curr)
     int d;  // split dim of curr, tracked incrementally (tree.hpp:27-29)
     // box mode: squared per-dimension offsets of curr's cell from the query,
     // and bit l set iff the path from level l went to the far child
@@ -424,6 +429,7 @@ struct LaneWalk {
         }
         curr = 1;  // 1-based ids inside the walk: the root, entered from its parent 0 (= -1)
         prev = 0;
+        fromp = true;
         d = 0;
         if constexpr (kBox) {
 #pragma unroll
@@ -439,7 +445,7 @@ struct LaneWalk {
     // in-register bounces.  Returns false once the root stepped to -1.
     __device__ __forceinline__ bool step(const WalkArgs& a) {
         const int32_t n = a.n;  // 1-based ids: node c exists iff c <= n
-        const bool from_parent = prev < curr;
+        const bool from_parent = kCarry ? fromp : prev < curr;
         const float* nodes = a.nodes - S;  // nodes + c * S is 1-based node c's slot
         float p[D];
         float pd;
@@ -523,8 +529,8 @@ struct LaneWalk {
         bool down;
         bool to_far = false, back_far = false;  // box mode: entering / leaving the far child
         if constexpr (!UNORDERED) {
-            const int32_t close = cs ? r : l;                      // 228
-            const int32_t far = cs ? l : r;                        // 229
+            const int32_t close = kCarry ? (l | int32_t(cs)) : (cs ? r : l);  // 228 (1-based: r = l | 1)
+            const int32_t far = kCarry ? (close ^ 1) : (cs ? l : r);           // 229
             // 232-238 with the bounces off empty slots (206-212) folded in:
             // from the parent, an empty close slot bounces straight back,
             // which is a return from the close child; an empty far slot
@@ -574,6 +580,7 @@ struct LaneWalk {
         }
         prev = curr;
         curr = next;
+        if constexpr (kCarry) fromp = down;
         return true;
     }
 
@@ -681,6 +688,7 @@ struct LaneWalk {
         const int2 st = a.wave_state[qi];  // 0-based (curr, prev)
         curr = st.x + 1;
         prev = st.y + 1;
+        fromp = prev < curr;
         d = depth_of(st.x) % D;
         if constexpr (kBox) box_recompute(a);
         if constexpr (kRot) {
