@@ -69,13 +69,23 @@ def main():
     buf = torch.zeros(cap * REC.itemsize // 8, dtype=torch.int64, device=dev)
     cnt = torch.zeros(1, dtype=torch.int64, device=dev)
     st = torch.cuda.current_stream()
-    for mode in ("serial", "concurrent"):
+    # the host path: one fkd_run_batches call, pinned buffers (bench.py's e2e)
+    qs_host = q.cpu().numpy()
+    hq = fk.LIB.fkd_host_alloc(qs_host.nbytes)
+    C.memmove(hq, qs_host.ctypes.data, qs_host.nbytes)
+    arr = (fk._lib.fkd_host_batch * 2)()
+    for i, o in enumerate(opts[::-1]):
+        arr[i].queries, arr[i].m, arr[i].dim, arr[i].opt = hq, m, 3, o.to_c()
+        arr[i].counts, arr[i].hits = fk.LIB.fkd_host_alloc(m * 4), fk.LIB.fkd_host_alloc(m * o.stride * 8)
+    for mode in ("serial", "concurrent", "host-grouped"):
         def step():
             if mode == "serial":
                 for (c, h), o in zip(outs, opts):
                     fk.run_batch_device(tree, q, c, h, o, stream=st)
-            else:
+            elif mode == "concurrent":
                 fk.run_batches_device(tree, [(q, c, h, o) for (c, h), o in zip(outs, opts)], stream=st)
+            else:
+                assert fk.LIB.fkd_run_batches(tree.handle, arr, 2) == 0
         for _ in range(3):
             step()
         torch.cuda.synchronize()
