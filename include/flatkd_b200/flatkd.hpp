@@ -242,6 +242,46 @@ inline BatchResult run_batch(const KdTree& tree, const PointSet& queries, const 
     return run_batch(tree, queries.raw().data(), queries.size(), queries.dim(), options);
 }
 
+// Several run_batch calls in one (fkd_run_batches): requests over the same
+// query array share its upload, finiteness check and Morton order, and their
+// walks overlap on the device.  Every result equals the run_batch one; the
+// first failing request's error is thrown after all have run.
+struct BatchRequest {
+    const float* queries = nullptr;
+    long long m = 0;
+    int dim = 0;
+    BatchOptions options;
+};
+
+inline std::vector<BatchResult> run_batches(const KdTree& tree, std::span<const BatchRequest> requests) {
+    std::vector<BatchResult> res(requests.size());
+    std::vector<fkd_host_batch> items(requests.size());
+    std::vector<fkd_query_stats> st(requests.size(), fkd_query_stats{0, 0, 0});
+    for (std::size_t i = 0; i < requests.size(); ++i) {
+        const BatchRequest& r = requests[i];
+        if (r.options.kind == QueryKind::knn && r.options.k < 1)
+            throw std::invalid_argument("knn: k must be >= 1");
+        res[i].stride = r.options.kind == QueryKind::knn ? r.options.k : 1;
+        res[i].counts.resize(static_cast<std::size_t>(r.m));
+        res[i].hits.resize(static_cast<std::size_t>(r.m) * res[i].stride);
+        items[i] = fkd_host_batch{r.queries, r.m, r.dim, r.options.to_c(), res[i].counts.data(),
+                                  reinterpret_cast<fkd_hit*>(res[i].hits.data()), &st[i], FKD_OK};
+    }
+    check(fkd_run_batches(tree.handle(), items.data(), static_cast<int32_t>(items.size())));
+    for (std::size_t i = 0; i < requests.size(); ++i)
+        if (requests[i].options.collect_stats)
+            res[i].stats = QueryStats{st[i].steps, st[i].nodes_visited, st[i].nodes_processed};
+    return res;
+}
+
+// The same queries under several option sets (fcp + kNN of one point set).
+inline std::vector<BatchResult> run_batches(const KdTree& tree, const PointSet& queries,
+                                            std::span<const BatchOptions> options) {
+    std::vector<BatchRequest> reqs;
+    for (const BatchOptions& o : options) reqs.push_back({queries.raw().data(), queries.size(), queries.dim(), o});
+    return run_batches(tree, std::span<const BatchRequest>(reqs));
+}
+
 namespace detail {
 
 // A traced single query: the GPU walks it with the literal state machine

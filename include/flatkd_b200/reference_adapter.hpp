@@ -74,4 +74,32 @@ inline flatkd::BatchResult run_batch(const KdTree& tree, const flatkd::PointSet&
     return res;
 }
 
+// Several flatkd::run_batch calls over one query set in one submission
+// (fkd_run_batches: one upload / finiteness check / Morton order, overlapped
+// walks); each result is the one flatkd::run_batch returns.
+inline std::vector<flatkd::BatchResult> run_batches(const KdTree& tree, const flatkd::PointSet& queries,
+                                                    std::span<const flatkd::BatchOptions> options) {
+    std::vector<flatkd::BatchResult> res(options.size());
+    std::vector<fkd_host_batch> items(options.size());
+    std::vector<fkd_query_stats> st(options.size(), fkd_query_stats{0, 0, 0});
+    const int m = queries.size();
+    for (std::size_t i = 0; i < options.size(); ++i) {
+        const flatkd::BatchOptions& o = options[i];
+        if (o.kind == flatkd::QueryKind::knn && o.k < 1) throw std::invalid_argument("knn: k must be >= 1");
+        res[i].stride = o.kind == flatkd::QueryKind::knn ? o.k : 1;
+        res[i].counts.assign(static_cast<std::size_t>(m), 0);
+        res[i].hits.assign(static_cast<std::size_t>(m) * res[i].stride, flatkd::Hit{});
+        items[i] = fkd_host_batch{queries.raw().data(), m, queries.dim(), to_c(o), res[i].counts.data(),
+                                  reinterpret_cast<fkd_hit*>(res[i].hits.data()), &st[i], FKD_OK};
+    }
+    check_ref(fkd_run_batches(tree.handle(), items.data(), static_cast<int32_t>(items.size())));
+    for (std::size_t i = 0; i < options.size(); ++i)
+        if (options[i].collect_stats) {
+            res[i].stats.steps = st[i].steps;
+            res[i].stats.nodes_visited = st[i].nodes_visited;
+            res[i].stats.nodes_processed = st[i].nodes_processed;
+        }
+    return res;
+}
+
 }  // namespace flatkd::b200

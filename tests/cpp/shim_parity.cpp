@@ -67,6 +67,38 @@ int main() {
         }
     }
 
+    // several option sets over one query set in one submission (run_batches)
+    {
+        std::vector<flatkd::BatchOptions> opts(4);
+        opts[1].kind = opts[2].kind = opts[3].kind = flatkd::QueryKind::knn;
+        opts[1].k = 8;
+        opts[2].k = 20;
+        opts[2].max_radius = 0.05f;
+        opts[3].k = 4;
+        opts[3].engine = flatkd::Engine::recursive;
+        for (auto& o : opts) o.collect_stats = true;
+        const auto gpu = flatkd::b200::run_batches(gpu_tree, queries, std::span<const flatkd::BatchOptions>(opts));
+        expect(gpu.size() == opts.size(), "run_batches result count");
+        for (std::size_t i = 0; i < opts.size() && i < gpu.size(); ++i) {
+            const auto ref = flatkd::run_batch(cpu_tree, queries, opts[i]);
+            expect(same(ref, gpu[i]), "run_batches results differ");
+            expect(ref.stats.steps == gpu[i].stats.steps && ref.stats.nodes_processed == gpu[i].stats.nodes_processed,
+                   "run_batches stats differ");
+        }
+        // the standalone shim's request form, two query arrays
+        flatkd::b200::BatchOptions bo;
+        bo.kind = flatkd::b200::QueryKind::knn;
+        bo.k = 5;
+        const std::vector<flatkd::b200::BatchRequest> reqs{
+            {queries.raw().data(), queries.size(), 3, bo},
+            {data.raw().data(), 3000, 3, flatkd::b200::BatchOptions{}}};
+        const auto two = flatkd::b200::run_batches(gpu_tree, std::span<const flatkd::b200::BatchRequest>(reqs));
+        for (int i = 0; i < 2; ++i) {
+            const auto one = flatkd::b200::run_batch(gpu_tree, reqs[i].queries, reqs[i].m, 3, reqs[i].options);
+            expect(one.counts == two[i].counts && one.hits == two[i].hits, "run_batches requests differ");
+        }
+    }
+
     // typed single-query entry points (float3-like struct) vs flatkd::fcp/knn
     for (int i = 0; i < 200; ++i) {
         const auto q = queries[i];

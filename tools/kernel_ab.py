@@ -46,7 +46,7 @@ def main():
         walk = float(np.median([t["walk_ms"] for t in ts[1:]]))
         print(json.dumps({"variant": v or "default", "dim": a.dim, "k": a.k, "m": a.m, "walk_ms": walk,
                           "qps": a.m / walk * 1e3, "tail_ms": float(np.median([t["tail_ms"] for t in ts[1:]])),
-                          "overflowed": ts[-1]["overflowed"], "same": got == ref}), flush=True)
+                          "overflowed": ts[-1]["overflowed"], "same": got == ref, "hash": f"{got:016x}"}), flush=True)
         for k_, v_ in old.items():
             if v_ is None:
                 os.environ.pop(k_, None)
