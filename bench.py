@@ -25,6 +25,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -412,9 +413,12 @@ def run_b200(args) -> None:
     # Pinned caller buffers (fkd_host_alloc) -> `e2e`; the drop-in as a
     # reference caller makes it (NumPy / std::vector, pageable) -> `e2e_pageable`.
     h2d = m * dim * 4 * (len(batches) if args.serial else 1)  # one upload per step when grouped
+    # an unbounded-radius batch's counts are min(k, n) for every query: the
+    # library writes them on the host (checked against the walked counts on
+    # the device) and copies only the hits
     d2h = 0
-    for kind, k, _ in batches:
-        d2h += m * 4 + m * k * 8
+    for kind, k, r in batches:
+        d2h += (m * 4 if math.isfinite(r) else 0) + m * k * 8
 
     def host_buffers(pinned: bool):
         bufs = {}
@@ -537,7 +541,8 @@ def run_b200(args) -> None:
                 "d2h_bytes_per_step": d2h, "results_equal_device_path": bool(e2e_parity),
                 "path": ("fkd_run_batch per batch" if args.serial else "one fkd_run_batches call per step (the "
                          "batches share the query array: one chunked pipeline, one upload)") +
-                        " (C ABI, pinned host buffers from fkd_host_alloc, chunked H2D/walk/D2H)"},
+                        " (C ABI, pinned host buffers from fkd_host_alloc, chunked H2D/walk/D2H; counts of "
+                        "unbounded-radius batches written on the host, verified on the device)"},
         "gpu_launches": launches // args.steps,
         "gpu_launches_note": "own kernels per timed step (per batch: Morton keys, walk, continuation "
                              "rounds (fcp: 3), resume pass, CTA overflow pass); CUB sort kernels excluded",

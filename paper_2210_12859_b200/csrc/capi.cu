@@ -55,6 +55,7 @@ struct BlockTraceConfig {
 BlockTraceConfig g_btrace;
 
 constexpr int kSmallWords = 64;   // per-workspace device counters (Workspace::small)
+constexpr int kCountFlag = 12;    // host pipeline: a walked count differed from the host-written one
 constexpr int kBatchTotals = 16;  // first per-batch totals word
 constexpr int kMaxGroup = (kSmallWords - kBatchTotals) / 3;  // batches per host pipeline
 
@@ -145,7 +146,7 @@ struct Workspace {
     void* sort_tmp = nullptr;
     size_t sort_tmp_bytes = 0;
     // [kSmallWords]: 0 bad, 1-3 steps/visited/processed, 5-6 ovf count/next,
-    // 8 resume count, 10 round count; from kBatchTotals: 3 totals per batch
+    // 8 resume count, 10 round count, 12 count flag; from kBatchTotals: 3 totals per batch
     // of a multi-batch host pipeline
     unsigned long long* small = nullptr;
     uint32_t* ovf = nullptr;                // overflow query ids
@@ -303,6 +304,18 @@ void par_copy(void* dst, const void* src, size_t bytes) {
         const size_t lo = std::min(bytes, size_t(i) * per), hi = std::min(bytes, lo + per);
         if (hi > lo) std::memcpy(static_cast<char*>(dst) + lo, static_cast<const char*>(src) + lo, hi - lo);
     });
+}
+
+void par_fill(int32_t* dst, int64_t count, int32_t v) {
+    if (count <= 0) return;
+    CopyPool& pool = CopyPool::get();
+    const int parts = count < (int64_t(1) << 20) ? 1 : pool.parts();
+    const int64_t per = ((count + parts - 1) / parts + 1023) & ~int64_t(1023);
+    auto part = [&](int i) {
+        const int64_t lo = std::min(count, int64_t(i) * per), hi = std::min(count, lo + per);
+        std::fill(dst + lo, dst + hi, v);
+    };
+    if (parts == 1) part(0); else pool.run(parts, part);
 }
 
 // First non-finite float of p[0, count) or -1 (require_finite, point.hpp:59-63:
@@ -1508,6 +1521,15 @@ fkd_status run_host_group(const fkd_tree* t, const float* queries, int64_t m, in
         out_bytes_per_query += 4.0 + 8.0 * g.k;
     }
     const bool check = t->n > 0;  // require_finite only with a non-empty tree (batch.cpp:75)
+    // Unbounded radius: every query gets exactly min(k, n) hits (trees and
+    // queries are finite, so every d2 passes d2 <= inf), so those counts are
+    // written on the host instead of copied (a third of an fcp batch's D2H
+    // bytes); a device pass over the walked counts raises an invariant error
+    // should one ever differ.
+    std::vector<int32_t> ccount(size_t(B), -1);
+    for (int b = 0; b < B; ++b)
+        if (kn.host_counts && t->n > 0 && std::isinf(batches[size_t(b)].cap2))
+            ccount[size_t(b)] = int32_t(std::min<int64_t>(batches[size_t(b)].k, t->n));
     const int ndev = int(t->reps.size());
     const int64_t per_dev = (m + ndev - 1) / ndev;
     // middle chunk = shard / div: 8 for kNN lists (D2H-bound: C3 kNN8 pinned
@@ -1631,6 +1653,7 @@ fkd_status run_host_group(const fkd_tree* t, const float* queries, int64_t m, in
         if (err == FKD_OK) {  // per-batch totals in slot 0's counter block
             cudaError_t e = cudaMemsetAsync(w0->small + kBatchTotals, 0, size_t(3 * B) * sizeof(unsigned long long),
                                             w0->stream);
+            if (e == cudaSuccess) e = cudaMemsetAsync(w0->small + kCountFlag, 0, sizeof(unsigned long long), w0->stream);
             if (e != cudaSuccess) err = fail(FKD_CUDA_ERROR, std::string("reset: ") + cudaGetErrorString(e));
         }
         pipes.push_back(std::move(P));
@@ -1740,6 +1763,12 @@ fkd_status run_host_group(const fkd_tree* t, const float* queries, int64_t m, in
                     stop = true;
                     break;
                 }
+                if (ccount[size_t(b)] >= 0 && check_counts(dc, jb.count, ccount[size_t(b)], io->small + kCountFlag,
+                                                           w->stream) < 0) {
+                    sh.error(FKD_CUDA_ERROR, "count check launch failed");
+                    stop = true;
+                    break;
+                }
                 if (b == 0 && B > 1 && use_morton(t, gb.o, jb.count) && jb.count <= kSortChunk)
                     share = SharedOrder{w->ids + w->key_cap / 2, w->small, P.ev_sorted[j]};
                 if (!cuda(cudaEventRecord(P.ev_walk[j], w->stream), "event")) {
@@ -1749,9 +1778,11 @@ fkd_status run_host_group(const fkd_tree* t, const float* queries, int64_t m, in
                 q_readers[size_t(first.ws)].push_back(j);
                 if (sharing) order_readers[size_t(first.ws)].push_back(j);
                 if (!P.pg_out) {
+                    if (ccount[size_t(b)] >= 0) par_fill(gb.counts + jb.base, jb.count, ccount[size_t(b)]);
                     if (!cuda(cudaStreamWaitEvent(io->cout, P.ev_walk[j], 0), "wait") ||
-                        !cuda(cudaMemcpyAsync(gb.counts + jb.base, dc, size_t(jb.count) * sizeof(int32_t),
-                                              cudaMemcpyDeviceToHost, io->cout), "D2H") ||
+                        (ccount[size_t(b)] < 0 &&
+                         !cuda(cudaMemcpyAsync(gb.counts + jb.base, dc, size_t(jb.count) * sizeof(int32_t),
+                                               cudaMemcpyDeviceToHost, io->cout), "D2H")) ||
                         !cuda(cudaMemcpyAsync(gb.hits + jb.base * gb.k, dh, size_t(jb.count) * gb.k * sizeof(fkd_hit),
                                               cudaMemcpyDeviceToHost, io->cout), "D2H") ||
                         !cuda(cudaEventRecord(P.ev_out[j], io->cout), "event")) {
@@ -1790,7 +1821,10 @@ fkd_status run_host_group(const fkd_tree* t, const float* queries, int64_t m, in
             }
             if (!ok || sh.stop) return;
             const char* slot = P.rst.p + (j % ring) * P.r_slot_bytes;
-            par_copy(gb.counts + jb.base, slot, size_t(jb.count) * sizeof(int32_t));
+            if (ccount[size_t(jb.b)] >= 0)
+                par_fill(gb.counts + jb.base, jb.count, ccount[size_t(jb.b)]);
+            else
+                par_copy(gb.counts + jb.base, slot, size_t(jb.count) * sizeof(int32_t));
             par_copy(gb.hits + jb.base * gb.k, slot + size_t(P.max_chunk) * sizeof(int32_t),
                      size_t(jb.count) * gb.k * sizeof(fkd_hit));
         };
@@ -1809,8 +1843,9 @@ fkd_status run_host_group(const fkd_tree* t, const float* queries, int64_t m, in
             job_results(P, jb, &dc, &dh);
             char* slot = P.rst.p + (j % ring) * P.r_slot_bytes;
             const bool good = cudaStreamWaitEvent(io->cout, P.ev_walk[j], 0) == cudaSuccess &&
-                              cudaMemcpyAsync(slot, dc, size_t(jb.count) * sizeof(int32_t), cudaMemcpyDeviceToHost,
-                                              io->cout) == cudaSuccess &&
+                              (ccount[size_t(jb.b)] >= 0 ||
+                               cudaMemcpyAsync(slot, dc, size_t(jb.count) * sizeof(int32_t), cudaMemcpyDeviceToHost,
+                                               io->cout) == cudaSuccess) &&
                               cudaMemcpyAsync(slot + size_t(P.max_chunk) * sizeof(int32_t), dh,
                                               size_t(jb.count) * gb.k * sizeof(fkd_hit), cudaMemcpyDeviceToHost,
                                               io->cout) == cudaSuccess &&
@@ -1842,13 +1877,11 @@ fkd_status run_host_group(const fkd_tree* t, const float* queries, int64_t m, in
     // ---- drain every stream, read the device flags and totals, release
     unsigned long long bad = kNoBad;
     std::vector<unsigned long long> tot(size_t(3 * B), 0ull);
+    bool count_differs = false;
     for (auto& P : pipes) {
         DeviceGuard g(P->rep->device);
-        for (Workspace* w : P->wss) {
-            cudaError_t e = cudaMemcpyAsync(w->h_small, w->small, kSmallWords * sizeof(unsigned long long),
-                                            cudaMemcpyDeviceToHost, w->stream);
-            if (e != cudaSuccess && err == FKD_OK) err = fail(FKD_CUDA_ERROR, std::string("readback: ") + cudaGetErrorString(e));
-        }
+        // every slot stream first: the batch totals and the count flag in
+        // slot 0's words are written by walks on all of them
         for (cudaStream_t cs : {P->wss[0]->cin, P->wss[0]->cout}) {
             cudaError_t e = cudaStreamSynchronize(cs);
             if (e != cudaSuccess && err == FKD_OK) err = fail(FKD_CUDA_ERROR, std::string("stream: ") + cudaGetErrorString(e));
@@ -1856,10 +1889,18 @@ fkd_status run_host_group(const fkd_tree* t, const float* queries, int64_t m, in
         for (Workspace* w : P->wss) {
             cudaError_t e = cudaStreamSynchronize(w->stream);
             if (e != cudaSuccess && err == FKD_OK) err = fail(FKD_CUDA_ERROR, std::string("stream: ") + cudaGetErrorString(e));
+        }
+        for (Workspace* w : P->wss) {
+            cudaError_t e = cudaMemcpyAsync(w->h_small, w->small, kSmallWords * sizeof(unsigned long long),
+                                            cudaMemcpyDeviceToHost, w->stream);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(w->stream);
+            if (e != cudaSuccess && err == FKD_OK) err = fail(FKD_CUDA_ERROR, std::string("readback: ") + cudaGetErrorString(e));
             if (err == FKD_OK && w->h_small[0] != kNoBad) bad = std::min(bad, (unsigned long long)w->h_small[0]);
         }
-        if (err == FKD_OK)
+        if (err == FKD_OK) {
             for (int i = 0; i < 3 * B; ++i) tot[size_t(i)] += P->wss[0]->h_small[kBatchTotals + i];
+            count_differs |= P->wss[0]->h_small[kCountFlag] != 0;
+        }
         if (P->ev_start && err == FKD_OK) {  // FKD_PIPE_TRACE: per-job timeline, ms from the first H2D
             for (size_t j = 0; j < P->jobs.size(); ++j) {
                 float tin = 0, tws = 0, tts = 0, tw = 0, tout = 0;
@@ -1889,6 +1930,8 @@ fkd_status run_host_group(const fkd_tree* t, const float* queries, int64_t m, in
     bad = std::min(bad, sh.host_bad);
     if (bad != kNoBad)
         return fail(FKD_DATA_ERROR, "queries: non-finite coordinate in point " + std::to_string(bad));
+    if (count_differs)
+        return fail(FKD_INVARIANT_ERROR, "unbounded-radius batch: a query's hit count differs from min(k, n)");
     for (int b = 0; b < B; ++b)
         if (batches[size_t(b)].stats)
             *batches[size_t(b)].stats = fkd_query_stats{int64_t(tot[size_t(3 * b)]), int64_t(tot[size_t(3 * b + 1)]),

@@ -45,6 +45,7 @@ Knobs read_knobs() {
     if (const char* e = std::getenv("FKD_PAGEABLE_STAGING")) k.pageable_staging = std::atoi(e) != 0;
     if (const char* e = std::getenv("FKD_HOST_RING")) k.host_ring = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("FKD_PIPE_TRACE")) k.pipe_trace = std::atoi(e) != 0;
+    if (const char* e = std::getenv("FKD_HOST_COUNTS")) k.host_counts = std::atoi(e) != 0;
     return k;
 }
 

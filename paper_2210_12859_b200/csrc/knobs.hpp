@@ -55,6 +55,10 @@ struct Knobs {
     bool pageable_staging = true;
     int host_ring = 4;
     bool pipe_trace = false;
+    // host pipeline: an unbounded-radius batch's counts (min(k, n) for every
+    // query) are written on the host and checked on the device instead of
+    // copied (FKD_HOST_COUNTS=0 copies them)
+    bool host_counts = true;
 };
 
 // A snapshot of the environment overrides on top of the defaults.

@@ -234,6 +234,30 @@ int scan_queries(const float* d_queries, int64_t m, int dim, unsigned long long*
     return 1;
 }
 
+// Sets *flag when some counts[i] != want.  The host pipeline writes the
+// counts of an unbounded-radius batch itself (every query then has exactly
+// min(k, n) hits: trees and queries are finite, so every distance passes
+// d2 <= inf) and copies only the hits; this pass proves the device agreed.
+__global__ void __launch_bounds__(256)
+    count_check_kernel(const int32_t* __restrict__ c, int64_t m, int32_t want, unsigned long long* flag) {
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    bool diff = false;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < m; i += stride)
+        diff |= __ldcs(c + i) != want;
+    if (__syncthreads_or(diff) && threadIdx.x == 0) atomicOr(flag, 1ull);
+}
+
+int check_counts(const int32_t* d_counts, int64_t m, int32_t want, unsigned long long* flag, cudaStream_t st) {
+    if (m <= 0) return 0;
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t blocks = (m + 255) / 256;
+    const unsigned grid = unsigned(std::max<int64_t>(1, std::min<int64_t>(blocks, int64_t(sms) * 4)));
+    count_check_kernel<<<grid, 256, 0, st>>>(d_counts, m, want, flag);
+    return 1;
+}
+
 // ---- tree store ----
 
 // level-order row-major [n x dim] -> padded [n x stride].  When the padding

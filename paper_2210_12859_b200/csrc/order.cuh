@@ -29,6 +29,9 @@ int morton_keys(const float* d_queries, int64_t m, int dim, const MortonFrame& f
 int scan_queries(const float* d_queries, int64_t m, int dim, unsigned long long* bad, int64_t id_base,
                  cudaStream_t st);
 
+// *flag |= 1 if any of d_counts[0, m) differs from want.
+int check_counts(const int32_t* d_counts, int64_t m, int32_t want, unsigned long long* flag, cudaStream_t st);
+
 int pack_nodes(const float* d_src, int64_t n, int dim, int stride, float* d_dst, cudaStream_t st);
 int tree_scan(const float* d_src, int64_t n, int dim, unsigned* d_lohi, unsigned long long* d_bad,
               cudaStream_t st);

@@ -713,7 +713,7 @@ def test_run_batches_device_concurrent_exact(oracle):
 
 @pytest.mark.parametrize("knobs", ["", "FKD_FULL_STAGING=0", "FKD_STREAMS=2;FKD_CHUNK_DIV=5",
                                    "FKD_FULL_STAGING=0;FKD_STREAMS=3;FKD_BUDGET=40;FKD_RESUME_MIN=50",
-                                   "FKD_PAGEABLE_STAGING=0"])
+                                   "FKD_PAGEABLE_STAGING=0", "FKD_HOST_COUNTS=0"])
 def test_run_batches_host_groups_exact(oracle, knobs, monkeypatch):
     """fkd_run_batches: batches over one query array run as one pipeline
     (shared upload, check and Morton order per chunk; full and ring device
@@ -756,6 +756,38 @@ def test_run_batches_host_groups_exact(oracle, knobs, monkeypatch):
         fk.LIB.fkd_host_free(hc)
         fk.LIB.fkd_host_free(hh)
     fk.LIB.fkd_host_free(hq)
+
+
+@pytest.mark.parametrize("knobs", ["", "FKD_FULL_STAGING=0;FKD_STREAMS=3", "FKD_PAGEABLE_STAGING=0"])
+def test_host_written_counts_unbounded_radius(oracle, knobs, monkeypatch):
+    """An unbounded-radius batch through the host pipeline: every count is
+    min(k, n), written on the host while only the hits are copied (the device
+    checks the walked counts); counts and hits equal the reference's with k
+    below and above n, for an infinite radius and one whose square overflows."""
+    import ctypes as C
+
+    for kv in filter(None, knobs.split(";")):
+        k_, v_ = kv.split("=")
+        monkeypatch.setenv(k_, v_)
+    q = fk.random_points(61, 2, 300_001, 3)
+    for n in (5, 3000):
+        nodes = oracle.build_tree(fk.random_points(61, 1, n, 3))
+        tree = fk.KdTree.from_level_order(nodes)
+        for kind, k, r in (("fcp", 1, INF), ("knn", 8, INF), ("knn", 3, 1e30), ("knn", 8, 0.05)):
+            o = fk.BatchOptions(kind=fk.QueryKind[kind], k=k, max_radius=r)
+            c, h, _, _ = oracle.run_batch(nodes, q, kind, k, r)
+            got = fk.run_batch(tree, q, o)  # pageable (NumPy) buffers
+            assert np.array_equal(got.counts, c) and got.hits.tobytes() == h.tobytes(), (n, kind, k, r)
+            m = len(q)  # pinned caller buffers
+            hq, hc, hh = fk.LIB.fkd_host_alloc(q.nbytes), fk.LIB.fkd_host_alloc(m * 4), fk.LIB.fkd_host_alloc(m * k * 8)
+            C.memmove(hq, q.ctypes.data, q.nbytes)
+            co = o.to_c()
+            assert fk.LIB.fkd_run_batch(tree.handle, hq, m, 3, C.byref(co), hc, hh, None) == 0
+            gc = np.ctypeslib.as_array(C.cast(C.c_void_p(hc), C.POINTER(C.c_int32)), shape=(m,))
+            gh = np.ctypeslib.as_array(C.cast(C.c_void_p(hh), C.POINTER(C.c_int64)), shape=(m * k,))
+            assert np.array_equal(gc, c) and gh.tobytes() == h.tobytes(), (n, kind, k, r)
+            for p in (hq, hc, hh):
+                fk.LIB.fkd_host_free(p)
 
 
 def test_run_batches_rejected_group_and_many_batches(oracle):
