@@ -6,6 +6,8 @@
 // No CPU fallback exists: every query is answered by the sm_100a kernels in
 // walk.cuh; without a usable device the calls fail with FKD_NO_DEVICE.
 #include <algorithm>
+#include <immintrin.h>
+#include <chrono>
 #include <atomic>
 #include <cmath>
 #include <memory>
@@ -231,10 +233,11 @@ struct DeviceGuard {
 // one copy at a time and blocks the host (21 GB/s D2H measured, and the
 // chunk pipeline serialises behind it: C3 kNN8 64 ms instead of 16 ms).
 // fkd_run_batch instead stages pageable buffers through pooled pinned
-// buffers of its own, moved by a small host copy pool (8 threads copy
-// pinned <-> warm pageable memory at ~74 GB/s, above the PCIe rate), so the
-// DMA engines stream exactly as with pinned caller buffers
-// (tools/micro/host_copy.cpp).
+// buffers of its own, moved by a host copy pool (up to 16 threads, streaming
+// stores: while the copy engine writes into pinned memory, 16 threads copy
+// pinned -> warm pageable memory at ~63 GB/s, above the PCIe rate), so the
+// DMA engines stream nearly as with pinned caller buffers
+// (tools/micro/host_copy.cpp, copy_contention.cpp).
 class CopyPool {
   public:
     static CopyPool& get() {
@@ -269,7 +272,12 @@ class CopyPool {
   private:
     CopyPool() {
         const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-        const int n = int(std::min(8u, std::max(1u, hw / 2))) - 1;  // + the calling thread
+        const int want = read_knobs().copy_threads;
+        // every hardware thread up to 16: with streaming stores the copy
+        // scales to 16 threads while the copy engine writes (C3 pageable
+        // call 29.5 -> 24.5-26.3 ms against 8 threads and memcpy,
+        // profiles/r02/r02ao_copy_pool_ab.log)
+        const int n = (want > 0 ? want : int(std::min(16u, hw))) - 1;  // + the calling thread
         for (int i = 0; i < n; ++i)
             workers_.emplace_back([this] {
                 for (;;) {
@@ -291,18 +299,52 @@ class CopyPool {
     std::vector<std::thread> workers_;
 };
 
+// memcpy with non-temporal (streaming) stores: the destination lines are
+// written whole without being read first (no read-for-ownership), which
+// glibc's memcpy does only above a size threshold the pool's per-thread
+// pieces stay under.  Falls back to memcpy without AVX2.
+__attribute__((target("avx2"))) void stream_copy_avx2(char* d, const char* s, size_t n) {
+    const size_t head = std::min(n, size_t((64 - (reinterpret_cast<uintptr_t>(d) & 63)) & 63));
+    std::memcpy(d, s, head);
+    d += head;
+    s += head;
+    n -= head;
+    size_t i = 0;
+    for (; i + 128 <= n; i += 128) {
+        const __m256i a = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(s + i));
+        const __m256i b = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(s + i + 32));
+        const __m256i c = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(s + i + 64));
+        const __m256i e = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(s + i + 96));
+        _mm256_stream_si256(reinterpret_cast<__m256i*>(d + i), a);
+        _mm256_stream_si256(reinterpret_cast<__m256i*>(d + i + 32), b);
+        _mm256_stream_si256(reinterpret_cast<__m256i*>(d + i + 64), c);
+        _mm256_stream_si256(reinterpret_cast<__m256i*>(d + i + 96), e);
+    }
+    std::memcpy(d + i, s + i, n - i);
+    _mm_sfence();
+}
+
+void copy_piece(char* d, const char* s, size_t n, bool stream) {
+    static const bool avx2 = __builtin_cpu_supports("avx2");
+    if (stream && avx2 && n >= (size_t(1) << 20))
+        stream_copy_avx2(d, s, n);
+    else
+        std::memcpy(d, s, n);
+}
+
 void par_copy(void* dst, const void* src, size_t bytes) {
     if (bytes == 0) return;
     CopyPool& pool = CopyPool::get();
+    static const bool stream = read_knobs().stream_copy;
     const int parts = bytes < (size_t(4) << 20) ? 1 : pool.parts();
     if (parts == 1) {
-        std::memcpy(dst, src, bytes);
+        copy_piece(static_cast<char*>(dst), static_cast<const char*>(src), bytes, stream);
         return;
     }
     const size_t per = ((bytes + parts - 1) / parts + 4095) & ~size_t(4095);
     pool.run(parts, [&](int i) {
         const size_t lo = std::min(bytes, size_t(i) * per), hi = std::min(bytes, lo + per);
-        if (hi > lo) std::memcpy(static_cast<char*>(dst) + lo, static_cast<const char*>(src) + lo, hi - lo);
+        if (hi > lo) copy_piece(static_cast<char*>(dst) + lo, static_cast<const char*>(src) + lo, hi - lo, stream);
     });
 }
 
@@ -1808,13 +1850,18 @@ fkd_status run_host_group(const fkd_tree* t, const float* queries, int64_t m, in
         Workspace* io = P.wss[0];
         const size_t ring = size_t(P.rring);
         bool gate = false, ok = false;
+        using clk = std::chrono::steady_clock;
+        const auto t_origin = clk::now();
+        auto ms_since = [&](clk::time_point t) { return std::chrono::duration<double, std::milli>(t - t_origin).count(); };
         auto copy_out = [&](size_t j) {
             const PipeJob& jb = P.jobs[j];
             const GroupBatch& gb = batches[size_t(jb.b)];
+            const auto t0 = clk::now();
             if (cudaEventSynchronize(P.ev_out[j]) != cudaSuccess) {
                 sh.error(FKD_CUDA_ERROR, "D2H failed");
                 return;
             }
+            const auto t1 = clk::now();
             if (!gate) {  // results reach the caller only once every query passed the check
                 ok = fused ? sh.wait_checks() : (sh.err == FKD_OK);
                 gate = true;
@@ -1827,6 +1874,10 @@ fkd_status run_host_group(const fkd_tree* t, const float* queries, int64_t m, in
                 par_copy(gb.counts + jb.base, slot, size_t(jb.count) * sizeof(int32_t));
             par_copy(gb.hits + jb.base * gb.k, slot + size_t(P.max_chunk) * sizeof(int32_t),
                      size_t(jb.count) * gb.k * sizeof(fkd_hit));
+            if (kn.pipe_trace)  // host side of the pageable drain, ms from the drain thread's start
+                std::fprintf(stderr, "dev %d job %zu copy-out wait %.3f-%.3f copy %.3f-%.3f (%.1f MB)\n", P.di, j,
+                             ms_since(t0), ms_since(t1), ms_since(t1), ms_since(clk::now()),
+                             double(jb.count) * (4.0 + 8.0 * gb.k) / 1e6);
         };
         size_t j = 0;
         for (;; ++j) {

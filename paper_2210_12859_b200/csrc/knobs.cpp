@@ -46,6 +46,8 @@ Knobs read_knobs() {
     if (const char* e = std::getenv("FKD_HOST_RING")) k.host_ring = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("FKD_PIPE_TRACE")) k.pipe_trace = std::atoi(e) != 0;
     if (const char* e = std::getenv("FKD_HOST_COUNTS")) k.host_counts = std::atoi(e) != 0;
+    if (const char* e = std::getenv("FKD_COPY_THREADS")) k.copy_threads = std::max(0, std::atoi(e));
+    if (const char* e = std::getenv("FKD_STREAM_COPY")) k.stream_copy = std::atoi(e) != 0;
     return k;
 }
 

@@ -59,6 +59,10 @@ struct Knobs {
     // query) are written on the host and checked on the device instead of
     // copied (FKD_HOST_COUNTS=0 copies them)
     bool host_counts = true;
+    // threads of the host copy pool (0: hardware threads, at most 16); read once
+    int copy_threads = 0;
+    // host copies with streaming stores (FKD_STREAM_COPY=0: memcpy); read once
+    bool stream_copy = true;
 };
 
 // A snapshot of the environment overrides on top of the defaults.
