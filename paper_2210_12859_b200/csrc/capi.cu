@@ -324,6 +324,16 @@ __attribute__((target("avx2"))) void stream_copy_avx2(char* d, const char* s, si
     _mm_sfence();
 }
 
+// std::fill with streaming stores (whole lines, no read-for-ownership).
+__attribute__((target("avx2"))) void stream_fill_avx2(int32_t* d, int64_t n, int32_t v) {
+    int64_t i = 0;
+    for (; i < n && (reinterpret_cast<uintptr_t>(d + i) & 31); ++i) d[i] = v;
+    const __m256i x = _mm256_set1_epi32(v);
+    for (; i + 8 <= n; i += 8) _mm256_stream_si256(reinterpret_cast<__m256i*>(d + i), x);
+    for (; i < n; ++i) d[i] = v;
+    _mm_sfence();
+}
+
 void copy_piece(char* d, const char* s, size_t n, bool stream) {
     static const bool avx2 = __builtin_cpu_supports("avx2");
     if (stream && avx2 && n >= (size_t(1) << 20))
@@ -353,9 +363,13 @@ void par_fill(int32_t* dst, int64_t count, int32_t v) {
     CopyPool& pool = CopyPool::get();
     const int parts = count < (int64_t(1) << 20) ? 1 : pool.parts();
     const int64_t per = ((count + parts - 1) / parts + 1023) & ~int64_t(1023);
+    static const bool stream = read_knobs().stream_copy && __builtin_cpu_supports("avx2");
     auto part = [&](int i) {
         const int64_t lo = std::min(count, int64_t(i) * per), hi = std::min(count, lo + per);
-        std::fill(dst + lo, dst + hi, v);
+        if (stream && hi - lo >= (int64_t(1) << 18))
+            stream_fill_avx2(dst + lo, hi - lo, v);
+        else
+            std::fill(dst + lo, dst + hi, v);
     };
     if (parts == 1) part(0); else pool.run(parts, part);
 }
