@@ -42,20 +42,39 @@ void set_carveout(K kernel) {
         cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, FKD_L1_CARVEOUT);
 }
 
+// Threads per walk block: kWalkThreads, or half of it when that keeps more
+// warps resident — a register count that strands part of the register file
+// in whole blocks (96 registers: 2 blocks of 256 = 16 warps per SM, but 5 of
+// 128 = 20).  N = 10M uniform: 4-D kNN20 9.09 -> 8.66 ms, kNN32 16.3 -> 14.9,
+// kNN64 25.1 -> 20.3, 3-D kNN32 5.97 -> 5.61; C3, kNN8/16/50 unchanged
+// (profiles/r02/r02at_walk_block_ab.log).
 template <class K>
-void launch_walk_grid(K kernel, const WalkArgs& a, unsigned grid, cudaStream_t st) {
+int pick_walk_threads(K kernel) {
+    int full = 0, half = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&full, kernel, kWalkThreads, 0) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&half, kernel, kWalkThreads / 2, 0) != cudaSuccess) {
+        cudaGetLastError();
+        return kWalkThreads;
+    }
+    return half * (kWalkThreads / 2) > full * kWalkThreads ? kWalkThreads / 2 : kWalkThreads;
+}
+
+template <class K>
+void launch_walk_grid(K kernel, const WalkArgs& a, int threads, cudaStream_t st) {
     set_carveout(kernel);
-    kernel<<<grid, kWalkThreads, 0, st>>>(a);
+    kernel<<<walk_blocks(a.m, threads), threads, 0, st>>>(a);
 }
 
 template <int D, int S, int KB, bool STATS, bool UNORDERED>
 void launch_one(const WalkArgs& a, cudaStream_t st) {
-    launch_walk_grid(walk_kernel<D, S, KB, STATS, UNORDERED>, a, walk_blocks(a.m, kWalkThreads), st);
+    static const int threads = pick_walk_threads(walk_kernel<D, S, KB, STATS, UNORDERED>);
+    launch_walk_grid(walk_kernel<D, S, KB, STATS, UNORDERED>, a, threads, st);
 }
 
 template <int D, int S, int KB, bool UNORDERED>
 void launch_round(const WalkArgs& a, cudaStream_t st) {
-    launch_walk_grid(walk_round_kernel<D, S, KB, UNORDERED>, a, walk_blocks(a.m, kWalkThreads), st);
+    static const int threads = pick_walk_threads(walk_round_kernel<D, S, KB, UNORDERED>);
+    launch_walk_grid(walk_round_kernel<D, S, KB, UNORDERED>, a, threads, st);
 }
 
 // phase 0: the walk kernel; phase 1: the overflow pass (when budgeted);
