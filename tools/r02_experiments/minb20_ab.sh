@@ -1,0 +1,7 @@
+for rep in 1 2; do
+for L in build/ab/lib_cur.so build/ab/lib_m20.so; do
+  for cfg in "--dim 4 --k 20 --m 2000000" "--dim 3 --k 20 --m 4000000" "--dim 2 --k 20 --m 4000000" "--dim 3 --k 20 --m 4000000 --clustered"; do
+    FKD_LIB=$L python tools/kernel_ab.py $cfg --reps 2 | sed "s|^|$(basename $L) |; s/\"tail_ms\": [0-9.]*, //" | cut -c1-150
+  done
+done
+done
