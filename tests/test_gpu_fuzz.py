@@ -2,6 +2,7 @@
 to 200k, dims 1..10, k in 1..100, random radii, grid snapping and duplicates,
 Morton on/off, both engines' counters — every batch bit-exact against the
 oracle (counts, hit nodes, dist2 bits, batch stats)."""
+import os
 import time
 
 import numpy as np
@@ -13,10 +14,12 @@ pytestmark = pytest.mark.gpu
 
 
 def test_random_sweep(oracle):
-    rng = oracle.instance_rng(20261018)
+    # FKD_FUZZ_SEED / FKD_FUZZ_SECONDS widen the sweep for a long run
+    rng = oracle.instance_rng(int(os.environ.get("FKD_FUZZ_SEED", "20261018")))
+    seconds = float(os.environ.get("FKD_FUZZ_SECONDS", "60"))
     t0 = time.time()
     cases = 0
-    while time.time() - t0 < 60 and cases < 400:
+    while time.time() - t0 < seconds and (cases < 400 or seconds > 60):
         n = rng.next_int(1, 200_000) if rng.chance(0.3) else rng.next_int(1, 5000)
         dim = rng.next_int(1, 10)
         grid = (0, 4, 8, 16, 1024)[rng.next_int(0, 4)]
@@ -39,6 +42,15 @@ def test_random_sweep(oracle):
         what = (cases, n, dim, grid, dup, m, kind, k, r, morton)
         assert np.array_equal(res.counts, c), what
         assert res.hits.tobytes() == h.tobytes(), what
+        if cases % 3 == 0:  # the device-resident entry point on the same batch
+            import torch
+
+            opts = fk.BatchOptions(kind=fk.QueryKind[kind], k=k, max_radius=r, morton=morton, engine=engine)
+            cd = torch.empty(len(qs), dtype=torch.int32, device="cuda")
+            hd = torch.empty(len(qs) * opts.stride, dtype=torch.int64, device="cuda")
+            fk.run_batch_device(tree, torch.from_numpy(qs).cuda(), cd, hd, opts)
+            assert np.array_equal(cd.cpu().numpy(), c), what
+            assert hd.cpu().numpy().tobytes() == h.tobytes(), what
         if res.stats.steps:
             assert (res.stats.steps, res.stats.nodes_visited, res.stats.nodes_processed) == \
                 (int(st["steps"]), int(st["nodes_visited"]), int(st["nodes_processed"])), what
