@@ -160,6 +160,19 @@ typedef struct fkd_host_batch {
  * results, counters and status; returns the first non-OK status. */
 fkd_status fkd_run_batches(const fkd_tree* tree, fkd_host_batch* batches, int32_t n);
 
+/* Asynchronous fkd_run_batches (a serving loop's submission): starts the
+ * batches on a library thread and returns at once with a job handle;
+ * fkd_wait joins the job, frees the handle and returns what fkd_run_batches
+ * would have (status fields, outputs and counters are valid from then on, and
+ * fkd_last_error on the waiting thread explains a failure).  Several jobs may
+ * be in flight on one tree: their pipelines share the device, so one job's
+ * uploads and walks overlap the previous job's result copies.  The batch
+ * array and every buffer it names must stay valid and untouched until
+ * fkd_wait returns. */
+typedef struct fkd_job fkd_job;
+fkd_status fkd_submit_batches(const fkd_tree* tree, fkd_host_batch* batches, int32_t n, fkd_job** job);
+fkd_status fkd_wait(fkd_job* job);
+
 /* Device buffers on the tree's first device, launched on `stream` (a
  * cudaStream_t; NULL = legacy default stream).  The kernels are enqueued on
  * `stream`; the call then synchronises that stream once, because the

@@ -41,7 +41,8 @@ __all__ = [
     "BatchOptions", "BatchResult", "DataError", "DeviceError", "Engine", "HIT_DTYPE",
     "InvalidArgument", "InvariantError", "KdTree", "QueryKind", "QueryStats", "build_tree",
     "build_level_order", "build_level_order_device", "clustered_points", "fcp", "knn", "random_points", "result_hash", "run_batch",
-    "run_batch_device", "run_batches", "run_batches_device", "morton_keys", "write_query_results", "LIB_PATH",
+    "run_batch_device", "run_batches", "run_batches_device", "submit_batches", "Job", "morton_keys",
+    "write_query_results", "LIB_PATH",
 ]
 
 HIT_DTYPE = np.dtype([("node", "<i4"), ("dist2", "<f4")])  # flatkd::Hit, 8 bytes
@@ -298,12 +299,9 @@ def run_batch(tree: KdTree, queries, options: Optional[BatchOptions] = None) -> 
     return BatchResult(stride, counts, hits, QueryStats.from_c(st) if options.collect_stats else QueryStats())
 
 
-def run_batches(tree: KdTree, batches) -> List[BatchResult]:
-    """Several host-buffer batches in one call (fkd_run_batches): ``batches``
-    is a list of (queries, BatchOptions).  Batches over the same query array
-    (the same object) run as one pipeline — the queries are uploaded, checked
-    and ordered once per chunk and walked by every batch.  Returns one
-    BatchResult per batch; raises on the first failing batch."""
+def _prepare_batches(tree: KdTree, batches):
+    """The fkd_host_batch array of run_batches / submit_batches, the arrays it
+    points into (kept alive by the caller) and the per-batch result parts."""
     n = len(batches)
     arr = (fkd_host_batch * max(n, 1))()
     keep, results = [], []
@@ -326,9 +324,52 @@ def run_batches(tree: KdTree, batches) -> List[BatchResult]:
         b = arr[i]
         b.queries, b.m, b.dim, b.opt = q.ctypes.data, m, dim, opt.to_c()
         b.counts, b.hits, b.stats = counts.ctypes.data, hits.ctypes.data, C.addressof(st)
-    _check(LIB.fkd_run_batches(tree.handle, arr, n))
+    return arr, keep, results
+
+
+def _batch_results(results) -> List[BatchResult]:
     return [BatchResult(opt.stride, c, h, QueryStats.from_c(st) if opt.collect_stats else QueryStats())
             for opt, c, h, st in results]
+
+
+def run_batches(tree: KdTree, batches) -> List[BatchResult]:
+    """Several host-buffer batches in one call (fkd_run_batches): ``batches``
+    is a list of (queries, BatchOptions).  Batches over the same query array
+    (the same object) run as one pipeline — the queries are uploaded, checked
+    and ordered once per chunk and walked by every batch.  Returns one
+    BatchResult per batch; raises on the first failing batch."""
+    arr, keep, results = _prepare_batches(tree, batches)
+    _check(LIB.fkd_run_batches(tree.handle, arr, len(batches)))
+    return _batch_results(results)
+
+
+class Job:
+    """A submission in flight (fkd_submit_batches); ``wait()`` returns its
+    BatchResults (or raises) once, and keeps the inputs alive until then."""
+
+    def __init__(self, tree, handle, arr, keep, results):
+        self._tree, self._handle, self._arr, self._keep, self._results = tree, handle, arr, keep, results
+
+    def wait(self) -> List[BatchResult]:
+        if self._handle is None:
+            raise InvalidArgument("job already waited for")
+        h, self._handle = self._handle, None
+        _check(LIB.fkd_wait(h))
+        return _batch_results(self._results)
+
+    def __del__(self):
+        if getattr(self, "_handle", None) is not None and LIB is not None:
+            LIB.fkd_wait(self._handle)  # never leave the library thread writing freed arrays
+
+
+def submit_batches(tree: KdTree, batches) -> Job:
+    """run_batches without waiting (fkd_submit_batches): returns a Job at
+    once; several jobs in flight on one tree overlap on the device (a serving
+    loop submits batch i+1 before collecting batch i)."""
+    arr, keep, results = _prepare_batches(tree, batches)
+    h = C.c_void_p()
+    _check(LIB.fkd_submit_batches(tree.handle, arr, len(batches), C.byref(h)))
+    return Job(tree, h, arr, keep, results)
 
 
 def _stream_ptr(stream):

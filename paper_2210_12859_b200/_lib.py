@@ -13,7 +13,7 @@ LIB_PATH = os.environ.get("FKD_LIB") or os.path.join(HERE, "libfkd_b200.so")  # 
 # every symbol include/fkd_b200.h declares
 EXPORTS = (
     "fkd_default_options", "fkd_tree_create", "fkd_tree_create_device", "fkd_tree_destroy",
-    "fkd_tree_size", "fkd_tree_dim", "fkd_tree_replicas", "fkd_tree_add_replicas", "fkd_morton_keys", "fkd_run_batch", "fkd_run_batches", "fkd_run_batch_device", "fkd_run_batches_device", "fkd_fcp", "fkd_knn",
+    "fkd_tree_size", "fkd_tree_dim", "fkd_tree_replicas", "fkd_tree_add_replicas", "fkd_morton_keys", "fkd_run_batch", "fkd_run_batches", "fkd_submit_batches", "fkd_wait", "fkd_run_batch_device", "fkd_run_batches_device", "fkd_fcp", "fkd_knn",
     "fkd_build_tree", "fkd_build_tree_device", "fkd_tree_build", "fkd_result_hash", "fkd_random_points", "fkd_clustered_points",
     "fkd_host_alloc", "fkd_host_free", "fkd_debug_block_trace", "fkd_last_error", "fkd_version", "fkd_trace_batch",
     "fkd_file_info", "fkd_read_file_device", "fkd_write_file", "fkd_tree_load",
@@ -71,6 +71,8 @@ def _load() -> C.CDLL:
     lib.fkd_run_batch_device.argtypes = [vp, vp, i64, i32, vp, vp, vp, vp, vp, vp, vp]
     lib.fkd_run_batches_device.argtypes = [vp, vp, i32, vp]
     lib.fkd_run_batches.argtypes = [vp, vp, i32]
+    lib.fkd_submit_batches.argtypes = [vp, vp, i32, vp]
+    lib.fkd_wait.argtypes = [vp]
     lib.fkd_fcp.argtypes = [vp, vp, i32, C.c_float, vp, vp, vp]
     lib.fkd_knn.argtypes = [vp, vp, i32, i32, C.c_float, vp, vp, vp]
     lib.fkd_build_tree.argtypes = [vp, i64, i32, vp]

@@ -19,6 +19,7 @@
 #include <functional>
 #include <mutex>
 #include <string>
+#include <new>
 #include <thread>
 #include <vector>
 
@@ -2091,6 +2092,47 @@ fkd_status fkd_run_batches(const fkd_tree* t, fkd_host_batch* batches, int32_t n
     }
     if (first != FKD_OK) return fail(first, first_msg);
     return FKD_OK;
+}
+
+// fkd_submit_batches / fkd_wait: fkd_run_batches on a thread of its own.  The
+// pipelines of concurrent jobs take their own workspaces (streams, staging)
+// from the replica pools, so nothing is shared but the device and the host
+// copy pool.
+struct fkd_job {
+    std::thread th;
+    fkd_status status = FKD_OK;
+    std::string err;
+};
+
+fkd_status fkd_submit_batches(const fkd_tree* t, fkd_host_batch* batches, int32_t n, fkd_job** job) {
+    if (!job) return fail(FKD_INVALID_ARGUMENT, "null job handle");
+    *job = nullptr;
+    if (n < 0 || (n > 0 && !batches)) return fail(FKD_INVALID_ARGUMENT, "bad batch list");
+    fkd_job* j = new (std::nothrow) fkd_job;
+    if (!j) return fail(FKD_CUDA_ERROR, "job allocation failed");
+    int dev = 0;
+    cudaGetDevice(&dev);  // the caller's current device, for the library thread
+    try {
+        j->th = std::thread([j, t, batches, n, dev] {
+            cudaSetDevice(dev);
+            j->status = fkd_run_batches(t, batches, n);
+            if (j->status != FKD_OK) j->err = fkd::g_err;
+        });
+    } catch (const std::exception& e) {
+        delete j;
+        return fail(FKD_CUDA_ERROR, std::string("job thread: ") + e.what());
+    }
+    *job = j;
+    return FKD_OK;
+}
+
+fkd_status fkd_wait(fkd_job* j) {
+    if (!j) return fail(FKD_INVALID_ARGUMENT, "null job");
+    j->th.join();
+    const fkd_status s = j->status;
+    if (s != FKD_OK) fkd::g_err = j->err;
+    delete j;
+    return s;
 }
 
 extern "C" {

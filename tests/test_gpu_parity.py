@@ -790,6 +790,34 @@ def test_host_written_counts_unbounded_radius(oracle, knobs, monkeypatch):
                 fk.LIB.fkd_host_free(p)
 
 
+def test_submit_batches_jobs_in_flight(oracle):
+    """fkd_submit_batches / fkd_wait: several jobs in flight on one tree
+    (their pipelines overlap on the device) each return exactly what
+    run_batches does; a job with a non-finite query fails at wait with the
+    reference's message, the others are unaffected; a job waits only once."""
+    pts = fk.clustered_points(71, 1, 60_000, 3)
+    tree = fk.KdTree.from_level_order(oracle.build_tree(pts))
+    qs = [fk.clustered_points(71, 2 + i, 400_000 + 1000 * i, 3) for i in range(3)]
+    bad = qs[1].copy()
+    bad[1234, 2] = np.inf
+    specs = [[(q, fk.BatchOptions(kind=fk.QueryKind.knn, k=8)), (q, fk.BatchOptions())] for q in qs]
+    jobs = [fk.submit_batches(tree, sp) for sp in specs]
+    bad_job = fk.submit_batches(tree, [(bad, fk.BatchOptions())])
+    more = fk.submit_batches(tree, [(qs[2], fk.BatchOptions(kind=fk.QueryKind.knn, k=20, max_radius=0.03))])
+    with pytest.raises(fk.DataError, match="non-finite coordinate in point 1234"):
+        bad_job.wait()
+    for sp, job in zip(specs, jobs):
+        got = job.wait()
+        ref = fk.run_batches(tree, sp)
+        for g, r in zip(got, ref):
+            assert np.array_equal(g.counts, r.counts) and g.hits.tobytes() == r.hits.tobytes()
+    (g,) = more.wait()
+    c, h, _, _ = oracle.run_batch(oracle.build_tree(pts), qs[2], "knn", 20, 0.03)
+    assert np.array_equal(g.counts, c) and g.hits.tobytes() == h.tobytes()
+    with pytest.raises(fk.InvalidArgument):
+        more.wait()
+
+
 def test_run_batches_rejected_group_and_many_batches(oracle):
     """A non-finite query rejects its whole group (same queries) with the
     first bad id and leaves pageable outputs untouched; another group's
