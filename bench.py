@@ -520,7 +520,9 @@ def run_b200(args) -> None:
                 if fk.LIB.fkd_wait(h) != 0:
                     raise RuntimeError(fk.LIB.fkd_last_error().decode())
 
-        run(max(depth, args.warmup))
+        # the first jobs in flight size their own workspaces (full-batch
+        # device staging per concurrent job): warm up past that
+        run(2 * depth + args.warmup)
         if dist is not None:
             dist.barrier()
         t0 = time.perf_counter()
