@@ -274,6 +274,75 @@ inline std::vector<BatchResult> run_batches(const KdTree& tree, std::span<const 
     return res;
 }
 
+// run_batches without blocking (fkd_submit_batches): the job owns its result
+// vectors; wait() joins it and returns them (or throws).  A serving loop
+// submits batch i+1 before waiting for batch i, so the device overlaps them.
+// The query arrays the requests point to must outlive wait().
+class Job {
+public:
+    Job() = default;
+    Job(const Job&) = delete;
+    Job& operator=(const Job&) = delete;
+    Job(Job&& o) noexcept { *this = std::move(o); }
+    Job& operator=(Job&& o) noexcept {
+        if (this != &o) {
+            finish();
+            h_ = o.h_;
+            o.h_ = nullptr;
+            res_ = std::move(o.res_);
+            items_ = std::move(o.items_);
+            st_ = std::move(o.st_);
+            want_stats_ = std::move(o.want_stats_);
+        }
+        return *this;
+    }
+    ~Job() { finish(); }
+
+    std::vector<BatchResult> wait() {
+        if (!h_) throw std::invalid_argument("job already waited for");
+        fkd_job* h = h_;
+        h_ = nullptr;
+        check(fkd_wait(h));
+        for (std::size_t i = 0; i < res_.size(); ++i)
+            if (want_stats_[i]) res_[i].stats = QueryStats{st_[i].steps, st_[i].nodes_visited, st_[i].nodes_processed};
+        return std::move(res_);
+    }
+
+private:
+    friend Job submit_batches(const KdTree& tree, std::span<const struct BatchRequest> requests);
+    void finish() {
+        if (h_) fkd_wait(h_);  // never leave the library thread writing freed vectors
+        h_ = nullptr;
+    }
+    fkd_job* h_ = nullptr;
+    std::vector<BatchResult> res_;
+    std::vector<fkd_host_batch> items_;
+    std::vector<fkd_query_stats> st_;
+    std::vector<char> want_stats_;
+};
+
+inline Job submit_batches(const KdTree& tree, std::span<const BatchRequest> requests) {
+    Job job;
+    job.res_.resize(requests.size());
+    job.items_.resize(requests.size());
+    job.st_.assign(requests.size(), fkd_query_stats{0, 0, 0});
+    job.want_stats_.resize(requests.size());
+    for (std::size_t i = 0; i < requests.size(); ++i) {
+        const BatchRequest& r = requests[i];
+        if (r.options.kind == QueryKind::knn && r.options.k < 1)
+            throw std::invalid_argument("knn: k must be >= 1");
+        BatchResult& res = job.res_[i];
+        res.stride = r.options.kind == QueryKind::knn ? r.options.k : 1;
+        res.counts.resize(static_cast<std::size_t>(r.m));
+        res.hits.resize(static_cast<std::size_t>(r.m) * res.stride);
+        job.want_stats_[i] = r.options.collect_stats;
+        job.items_[i] = fkd_host_batch{r.queries, r.m, r.dim, r.options.to_c(), res.counts.data(),
+                                       reinterpret_cast<fkd_hit*>(res.hits.data()), &job.st_[i], FKD_OK};
+    }
+    check(fkd_submit_batches(tree.handle(), job.items_.data(), static_cast<int32_t>(job.items_.size()), &job.h_));
+    return job;
+}
+
 // The same queries under several option sets (fcp + kNN of one point set).
 inline std::vector<BatchResult> run_batches(const KdTree& tree, const PointSet& queries,
                                             std::span<const BatchOptions> options) {

@@ -97,6 +97,14 @@ int main() {
             const auto one = flatkd::b200::run_batch(gpu_tree, reqs[i].queries, reqs[i].m, 3, reqs[i].options);
             expect(one.counts == two[i].counts && one.hits == two[i].hits, "run_batches requests differ");
         }
+        // asynchronous submission: two jobs in flight, collected in order
+        auto j1 = flatkd::b200::submit_batches(gpu_tree, std::span<const flatkd::b200::BatchRequest>(reqs));
+        auto j2 = flatkd::b200::submit_batches(gpu_tree, std::span<const flatkd::b200::BatchRequest>(reqs));
+        const auto a1 = j1.wait();
+        const auto a2 = j2.wait();
+        for (int i = 0; i < 2; ++i)
+            expect(a1[i].counts == two[i].counts && a1[i].hits == two[i].hits && a2[i].hits == two[i].hits,
+                   "submit_batches results differ");
     }
 
     // typed single-query entry points (float3-like struct) vs flatkd::fcp/knn
