@@ -546,7 +546,11 @@ def run_b200(args) -> None:
 
     e2e_value, e2e_parity = e2e_run(True)
     e2e_pg_value, e2e_pg_parity = e2e_run(False) if not args.no_pageable else (None, None)
-    e2e_pp_value, e2e_pp_parity = e2e_pipelined_run() if not args.serial else (None, None)
+    # the serving loop is for batches a server pipelines; two 1B-query C5
+    # jobs in flight hold twice the full-batch staging and measured slower
+    # than one (2.35 vs 2.93 G q/s, profiles/r02/r02bc_bench_c5.json)
+    pipelined = not args.serial and m <= (1 << 27)
+    e2e_pp_value, e2e_pp_parity = e2e_pipelined_run() if pipelined else (None, None)
 
     if rank != 0:
         if dist is not None:
