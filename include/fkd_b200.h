@@ -166,9 +166,9 @@ fkd_status fkd_run_batches(const fkd_tree* tree, fkd_host_batch* batches, int32_
  * would have (status fields, outputs and counters are valid from then on, and
  * fkd_last_error on the waiting thread explains a failure).  Several jobs may
  * be in flight on one tree: their pipelines share the device, so one job's
- * uploads and walks overlap the previous job's result copies.  The batch
- * array and every buffer it names must stay valid and untouched until
- * fkd_wait returns. */
+ * uploads and walks overlap the previous job's result copies.  The tree, the
+ * batch array and every buffer it names must stay valid (the buffers
+ * untouched) until fkd_wait returns; every job must be waited for once. */
 typedef struct fkd_job fkd_job;
 fkd_status fkd_submit_batches(const fkd_tree* tree, fkd_host_batch* batches, int32_t n, fkd_job** job);
 fkd_status fkd_wait(fkd_job* job);
