@@ -62,7 +62,9 @@ constexpr int kCountFlag = 12;    // host pipeline: a walked count differed from
 constexpr int kBatchTotals = 16;  // first per-batch totals word
 constexpr int kMaxGroup = (kSmallWords - kBatchTotals) / 3;  // batches per host pipeline
 
+constexpr int kMaxRegDim = 16;  // dims with compile-time walk kernels (larger: the heap kernel)
 int walk_bucket_of(int k);
+int walk_bucket_of(int k, int dim, bool stats = false, bool unordered = false);
 // The rounds run for register lists of <= 4 slots (fcp, k <= 4) and, in
 // batches of >= 2^22 queries, 8 slots (a 1M-query kNN8 batch is 4-8% slower
 // with them: the round boundaries cost more than the small batch's warps lose).
@@ -76,8 +78,14 @@ inline bool rounds_on(int k, int64_t m, const Knobs& kn, int dim) {
     if (dim >= kLongWalkDim && k > 1) return false;
     return kb <= 4 || (kb == 8 && m >= kn.rounds_min_m);
 }
-// first walk's loop trips before a query parks (FKD_BUDGET < 0: per kind)
+// From 12-D nearly every walk outgrows any first budget, and parking them
+// all only to finish them in the resume / CTA passes costs more than one
+// walk to the end (M = 1M, N = 1M: 12-D kNN8 1026 -> 846 ms, 16-D 21.1 ->
+// 5.8 s; 10-D keeps the budget, 37 vs 49 ms; profiles/r02/r02bd_hd_budget_ab.log)
+constexpr int kNoBudgetDim = 12;
+// first walk's loop trips before a query parks (FKD_BUDGET < 0: per kind; 0: no budget)
 inline int first_budget(int k, int64_t m, const Knobs& kn, int dim) {
+    if (dim >= kNoBudgetDim) return 0;
     if (dim >= kLongWalkDim) return k == 1 ? 1024 : 8192;
     if (k == 1) return 112;
     if (!rounds_on(k, m, kn, dim)) return 3072;
@@ -131,6 +139,8 @@ int store_stride(int dim) {
         case 3: return packed ? 3 : 4;
         case 4: return 4;
         case 5: case 6: case 7: case 8: return 8;
+        case 9: case 10: case 11: return 12;  // three 16-byte vectors, the split plane in the last float
+        case 12: case 13: case 14: case 15: case 16: return 16;
         default: return dim;
     }
 }
@@ -575,6 +585,15 @@ void release_ws(Replica& r, Workspace* w) {
 #ifndef FKD_REG_MAXK
 #define FKD_REG_MAXK 64
 #endif
+// Register-list walks exist for dims 1..kMaxRegDim; dims 9..16 carry the
+// buckets 1 / 8 / 16 / 32 / 64 only (k rounds up; the unused leading slots
+// hold the dummy key), which keeps their eight kernel sets small.
+int walk_bucket_of(int k, int dim, bool stats, bool unordered) {
+    if (k > FKD_REG_MAXK || dim > kMaxRegDim) return 0;
+    if (dim > 8 && (stats || unordered)) return 0;  // 9..16-D register walks: production (ordered) only
+    if (dim > 8) return k <= 1 ? 1 : (k <= 8 ? 8 : (k <= 16 ? 16 : (k <= 32 ? 32 : 64)));
+    return walk_bucket_of(k);
+}
 int walk_bucket_of(int k) {
     if (k > FKD_REG_MAXK) return 0;
     if (k <= 1) return 1;
@@ -613,7 +632,7 @@ fkd_status validate(const fkd_tree* t, int64_t m, int32_t dim, const fkd_batch_o
 bool use_morton(const fkd_tree* t, const fkd_batch_options* o, int64_t m) {
     if (o->flags & FKD_FLAG_NO_MORTON) return false;
     if (!(o->flags & FKD_FLAG_MORTON)) return false;
-    return t->n > 0 && m > 1 && t->dim <= 8;
+    return t->n > 0 && m > 1 && t->dim <= kMaxRegDim;  // from 9-D the key covers the first 8 axes
 }
 
 // A Morton order computed by another batch of the same submission over the
@@ -672,7 +691,7 @@ fkd_status enqueue(const fkd_tree* t, Replica& r, Workspace* w, const float* d_q
     // walk writes a slot: the key pass checks each sub-batch it sorts; a batch
     // of several sub-batches, or one walked without the key pass, is scanned
     // first.  The walk kernels exit at entry once *bad is set.
-    if ((!sort || m > chunk) && !(share && share->order)) {
+    if ((!sort || m > chunk || t->dim > 8) && !(share && share->order)) {  // from 9-D the key pass reads 8 axes
         *launches += scan_queries(d_q, m, t->dim, w->small, id_offset, st);
         FKD_CUDA(cudaGetLastError());
     }
@@ -700,7 +719,7 @@ fkd_status enqueue(const fkd_tree* t, Replica& r, Workspace* w, const float* d_q
         a.id_base = id_offset + base;
         int budget = tu.budget >= 0 ? tu.budget : first_budget(k, cm, tu, t->dim);
         if (budget_div > 1 && budget > 0) budget = std::max(64, budget / budget_div);
-        a.budget = (stats || walk_bucket_of(k) == 0 || t->dim > 8) ? 0 : budget;
+        a.budget = (stats || walk_bucket_of(k, t->dim, stats, (o->flags & FKD_FLAG_UNORDERED) != 0) == 0) ? 0 : budget;
         if (a.budget > 0) {
             FKD_CUDA(grow(w->ovf, w->ovf_cap, cm));
             FKD_CUDA(grow(w->wave_state, w->wave_state_cap, cm));
@@ -807,8 +826,8 @@ int walk_bucket(int k) { return walk_bucket_of(k); }
 
 int launch_walk(const WalkArgs& a, int dim, int stride, bool stats, bool unordered, int phase,
                 cudaStream_t st) {
-    const int KB = walk_bucket_of(a.k);
-    if (KB == 0 || dim > 8) return phase == 0 ? launch_walk_heap(a, dim, stats, unordered, st) : 0;
+    const int KB = walk_bucket_of(a.k, dim, stats, unordered);
+    if (KB == 0) return phase == 0 ? launch_walk_heap(a, dim, stats, unordered, st) : 0;
     switch (dim) {
         case 1: return launch_walk_d1(a, stride, KB, stats, unordered, phase, st);
         case 2: return launch_walk_d2(a, stride, KB, stats, unordered, phase, st);
@@ -818,6 +837,14 @@ int launch_walk(const WalkArgs& a, int dim, int stride, bool stats, bool unorder
         case 6: return launch_walk_d6(a, stride, KB, stats, unordered, phase, st);
         case 7: return launch_walk_d7(a, stride, KB, stats, unordered, phase, st);
         case 8: return launch_walk_d8(a, stride, KB, stats, unordered, phase, st);
+        case 9: return launch_walk_d9(a, stride, KB, stats, unordered, phase, st);
+        case 10: return launch_walk_d10(a, stride, KB, stats, unordered, phase, st);
+        case 11: return launch_walk_d11(a, stride, KB, stats, unordered, phase, st);
+        case 12: return launch_walk_d12(a, stride, KB, stats, unordered, phase, st);
+        case 13: return launch_walk_d13(a, stride, KB, stats, unordered, phase, st);
+        case 14: return launch_walk_d14(a, stride, KB, stats, unordered, phase, st);
+        case 15: return launch_walk_d15(a, stride, KB, stats, unordered, phase, st);
+        case 16: return launch_walk_d16(a, stride, KB, stats, unordered, phase, st);
         default: return 0;
     }
 }
@@ -856,13 +883,12 @@ int32_t fkd_tree_dim(const fkd_tree* t) { return t ? t->dim : 0; }
 fkd_status fkd_morton_keys(const fkd_tree* t, const float* d_queries, int64_t m, int32_t dim, uint32_t* d_keys,
                            int32_t* key_bits, void* stream) {
     if (!t) return fail(FKD_INVALID_ARGUMENT, "null tree");
-    if (key_bits) *key_bits = t->n > 0 && t->dim <= 8 ? t->frame.bits * t->dim : 0;
+    if (key_bits) *key_bits = t->n > 0 ? t->frame.bits * std::min(t->dim, 8) : 0;
     if (m < 0) return fail(FKD_INVALID_ARGUMENT, "negative query count");
     if (m == 0 || t->n == 0) return FKD_OK;
     if (dim != t->dim)
         return fail(FKD_DATA_ERROR, "query dimension " + std::to_string(dim) + " does not match tree dimension " +
                                         std::to_string(t->dim));
-    if (t->dim > 8) return fail(FKD_INVALID_ARGUMENT, "Morton keys exist for dim <= 8");
     if (t->reps.empty()) return fail(FKD_NO_DEVICE, "tree has no device replica");
     DeviceGuard g(t->reps[0]->device);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -870,6 +896,7 @@ fkd_status fkd_morton_keys(const fkd_tree* t, const float* d_queries, int64_t m,
     FKD_CUDA(cudaMallocAsync(&bad, sizeof(unsigned long long), st));
     FKD_CUDA(cudaMemsetAsync(bad, 0xFF, sizeof(unsigned long long), st));
     if (morton_keys(d_queries, m, dim, t->frame, d_keys, bad, st) < 0) return fail(FKD_CUDA_ERROR, "morton keys");
+    if (dim > 8) scan_queries(d_queries, m, dim, bad, 0, st);  // the key reads the first 8 axes
     FKD_CUDA(cudaGetLastError());
     unsigned long long h = 0;
     FKD_CUDA(cudaMemcpyAsync(&h, bad, sizeof(h), cudaMemcpyDeviceToHost, st));

@@ -43,8 +43,10 @@ int morton_bits_per_dim(int dim) {
 // query id goes to *bad (atomicMin), and the walk kernels that follow exit
 // at entry when *bad is set, so no result slot is written for a rejected
 // batch (the reference throws before its BatchResult exists, :82-86).
+// D axes of a query stored qs floats apart (qs = D, or the query dimension
+// from 9-D up, where the key covers the first 8 axes and a scan checks the rest)
 template <int D>
-__device__ __forceinline__ uint32_t morton_key(const float* __restrict__ q, int64_t i, const MortonFrame& f,
+__device__ __forceinline__ uint32_t morton_key(const float* __restrict__ q, int64_t i, int qs, const MortonFrame& f,
                                                unsigned long long* bad, int64_t id_base) {
     const int b = f.bits;
     const float top = float((1u << b) - 1u);
@@ -52,7 +54,7 @@ __device__ __forceinline__ uint32_t morton_key(const float* __restrict__ q, int6
     bool finite = true;
 #pragma unroll
     for (int d = 0; d < D; ++d) {
-        const float v = __ldg(q + i * D + d);
+        const float v = __ldg(q + i * qs + d);
         finite &= isfinite(v);
         float t = (v - f.lo[d]) * f.scale[d];
         t = fminf(fmaxf(t, 0.0f), top);  // NaN -> 0 (the batch is rejected anyway)
@@ -70,12 +72,12 @@ __device__ __forceinline__ uint32_t morton_key(const float* __restrict__ q, int6
 // counting sort, pass 1: key + rank inside the key's bin
 template <int D>
 __global__ void __launch_bounds__(256)
-    morton_rank_kernel(const float* __restrict__ q, int64_t m, MortonFrame f, uint32_t* __restrict__ bins,
+    morton_rank_kernel(const float* __restrict__ q, int64_t m, int qs, MortonFrame f, uint32_t* __restrict__ bins,
                        uint32_t* __restrict__ keys, uint32_t* __restrict__ ranks, unsigned long long* bad,
                        int64_t id_base) {
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= m) return;
-    const uint32_t key = morton_key<D>(q, i, f, bad, id_base);
+    const uint32_t key = morton_key<D>(q, i, qs, f, bad, id_base);
     keys[i] = key;
     ranks[i] = atomicAdd(bins + key, 1u);
 }
@@ -92,7 +94,8 @@ __global__ void __launch_bounds__(256)
 namespace {
 constexpr size_t kAlign = 256;
 size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
-int64_t key_bins(int dim) { return int64_t(1) << (morton_bits_per_dim(dim) * dim); }
+int key_axes(int dim) { return dim < 8 ? dim : 8; }
+int64_t key_bins(int dim) { return int64_t(1) << (morton_bits_per_dim(key_axes(dim)) * key_axes(dim)); }
 // Counting sort from 2^20 (below, scanning the bins dominates) to 2^25
 // queries (above, the rank atomics are L2-atomic-throughput bound: 1B
 // uniform queries order in 68 ms this way against 32 ms for the onesweep).
@@ -103,7 +106,7 @@ int64_t key_bins(int dim) { return int64_t(1) << (morton_bits_per_dim(dim) * dim
 #define FKD_COUNT_SORT_MAX (int64_t(1) << 25)
 #endif
 bool use_counting(int64_t m, int dim) {
-    return m >= FKD_COUNT_SORT_MIN && m <= FKD_COUNT_SORT_MAX && dim >= 1 && dim <= 8;
+    return m >= FKD_COUNT_SORT_MIN && m <= FKD_COUNT_SORT_MAX && dim >= 1 && dim <= 16;
 }
 size_t scan_bytes(int64_t bins) {
     size_t bytes = 0;
@@ -115,12 +118,12 @@ size_t scan_bytes(int64_t bins) {
 // radix path: keys + ids for the onesweep
 template <int D>
 __global__ void __launch_bounds__(256)
-    morton_keys_kernel(const float* __restrict__ q, int64_t m, MortonFrame f,
+    morton_keys_kernel(const float* __restrict__ q, int64_t m, int qs, MortonFrame f,
                        uint32_t* __restrict__ keys, uint32_t* __restrict__ ids, unsigned long long* bad,
                        int64_t id_base) {
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= m) return;
-    keys[i] = morton_key<D>(q, i, f, bad, id_base);
+    keys[i] = morton_key<D>(q, i, qs, f, bad, id_base);
     ids[i] = uint32_t(i);
 }
 
@@ -128,19 +131,19 @@ __global__ void __launch_bounds__(256)
 // partition (paper_2210_12859_b200/shard.py) splits a batch by these keys
 template <int D>
 __global__ void __launch_bounds__(256)
-    morton_keys_only_kernel(const float* __restrict__ q, int64_t m, MortonFrame f, uint32_t* __restrict__ keys,
+    morton_keys_only_kernel(const float* __restrict__ q, int64_t m, int qs, MortonFrame f, uint32_t* __restrict__ keys,
                             unsigned long long* bad) {
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= m) return;
-    keys[i] = morton_key<D>(q, i, f, bad, 0);
+    keys[i] = morton_key<D>(q, i, qs, f, bad, 0);
 }
 
 int morton_keys(const float* d_queries, int64_t m, int dim, const MortonFrame& f, uint32_t* keys,
                 unsigned long long* bad, cudaStream_t st) {
     if (m <= 0) return 0;
     const unsigned grid = unsigned((m + 255) / 256);
-    switch (dim) {
-#define FKD_KEYS(D) case D: morton_keys_only_kernel<D><<<grid, 256, 0, st>>>(d_queries, m, f, keys, bad); break;
+    switch (key_axes(dim)) {
+#define FKD_KEYS(D) case D: morton_keys_only_kernel<D><<<grid, 256, 0, st>>>(d_queries, m, dim, f, keys, bad); break;
         FKD_KEYS(1) FKD_KEYS(2) FKD_KEYS(3) FKD_KEYS(4) FKD_KEYS(5) FKD_KEYS(6) FKD_KEYS(7) FKD_KEYS(8)
 #undef FKD_KEYS
         default: return -1;
@@ -167,7 +170,10 @@ int morton_order(const float* d_queries, int64_t m, int dim, const MortonFrame& 
     // 10M queries -> 8 bits per axis, a 1.25M host-path chunk -> 7, where 8
     // costs 0.092 vs 0.055 ms of ordering for the same walk time).
     MortonFrame f = frame;
-    if (dim >= 1 && dim <= 8 && m > 0) {
+    const int qs = dim;
+    const bool counting = use_counting(m, dim);
+    dim = key_axes(dim);  // from here on: the key's axes
+    if (dim >= 1 && m > 0) {
         const int fit = int(std::floor(std::log2(double(m) * 1.7) / dim));
         const int b = std::max(1, std::min(frame.bits, fit));
         if (b < frame.bits) {
@@ -176,7 +182,7 @@ int morton_order(const float* d_queries, int64_t m, int dim, const MortonFrame& 
             f.bits = b;
         }
     }
-    if (use_counting(m, dim)) {
+    if (counting) {
         const int64_t bins = int64_t(1) << (f.bits * dim);  // <= key_bins(dim), which sized temp
         uint32_t* cnt = static_cast<uint32_t*>(temp);
         uint32_t* offs = reinterpret_cast<uint32_t*>(static_cast<char*>(temp) + align_up(size_t(bins) * 4));
@@ -186,7 +192,7 @@ int morton_order(const float* d_queries, int64_t m, int dim, const MortonFrame& 
         if (cudaMemsetAsync(cnt, 0, size_t(bins) * 4, st) != cudaSuccess) return -1;
         uint32_t* ranks = keys_out;
         switch (dim) {
-#define FKD_RANK(D) case D: morton_rank_kernel<D><<<grid, 256, 0, st>>>(d_queries, m, f, cnt, keys_in, ranks, bad, id_base); break;
+#define FKD_RANK(D) case D: morton_rank_kernel<D><<<grid, 256, 0, st>>>(d_queries, m, qs, f, cnt, keys_in, ranks, bad, id_base); break;
             FKD_RANK(1) FKD_RANK(2) FKD_RANK(3) FKD_RANK(4) FKD_RANK(5) FKD_RANK(6) FKD_RANK(7) FKD_RANK(8)
 #undef FKD_RANK
             default: return -1;
@@ -196,14 +202,14 @@ int morton_order(const float* d_queries, int64_t m, int dim, const MortonFrame& 
         return 2;  // our own launches (the scan is a library launch)
     }
     switch (dim) {
-        case 1: morton_keys_kernel<1><<<grid, 256, 0, st>>>(d_queries, m, f, keys_in, ids_in, bad, id_base); break;
-        case 2: morton_keys_kernel<2><<<grid, 256, 0, st>>>(d_queries, m, f, keys_in, ids_in, bad, id_base); break;
-        case 3: morton_keys_kernel<3><<<grid, 256, 0, st>>>(d_queries, m, f, keys_in, ids_in, bad, id_base); break;
-        case 4: morton_keys_kernel<4><<<grid, 256, 0, st>>>(d_queries, m, f, keys_in, ids_in, bad, id_base); break;
-        case 5: morton_keys_kernel<5><<<grid, 256, 0, st>>>(d_queries, m, f, keys_in, ids_in, bad, id_base); break;
-        case 6: morton_keys_kernel<6><<<grid, 256, 0, st>>>(d_queries, m, f, keys_in, ids_in, bad, id_base); break;
-        case 7: morton_keys_kernel<7><<<grid, 256, 0, st>>>(d_queries, m, f, keys_in, ids_in, bad, id_base); break;
-        case 8: morton_keys_kernel<8><<<grid, 256, 0, st>>>(d_queries, m, f, keys_in, ids_in, bad, id_base); break;
+        case 1: morton_keys_kernel<1><<<grid, 256, 0, st>>>(d_queries, m, qs, f, keys_in, ids_in, bad, id_base); break;
+        case 2: morton_keys_kernel<2><<<grid, 256, 0, st>>>(d_queries, m, qs, f, keys_in, ids_in, bad, id_base); break;
+        case 3: morton_keys_kernel<3><<<grid, 256, 0, st>>>(d_queries, m, qs, f, keys_in, ids_in, bad, id_base); break;
+        case 4: morton_keys_kernel<4><<<grid, 256, 0, st>>>(d_queries, m, qs, f, keys_in, ids_in, bad, id_base); break;
+        case 5: morton_keys_kernel<5><<<grid, 256, 0, st>>>(d_queries, m, qs, f, keys_in, ids_in, bad, id_base); break;
+        case 6: morton_keys_kernel<6><<<grid, 256, 0, st>>>(d_queries, m, qs, f, keys_in, ids_in, bad, id_base); break;
+        case 7: morton_keys_kernel<7><<<grid, 256, 0, st>>>(d_queries, m, qs, f, keys_in, ids_in, bad, id_base); break;
+        case 8: morton_keys_kernel<8><<<grid, 256, 0, st>>>(d_queries, m, qs, f, keys_in, ids_in, bad, id_base); break;
         default: return -1;
     }
     size_t bytes = temp_bytes;

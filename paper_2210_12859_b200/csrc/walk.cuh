@@ -232,6 +232,23 @@ __device__ __forceinline__ void load_point(const float* __restrict__ nodes, int3
 #pragma unroll
         for (int j = 0; j < D; ++j) p[j] = t[j];
         if (split) *split = t[7];
+    } else if constexpr (S == 12 || S == 16) {
+        // 9..16-D: three or four 16-byte vectors; with S > D the last float is the split plane
+        constexpr int NV = S / 4;
+        float t[S];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+            const float4 x = __ldg(reinterpret_cast<const float4*>(base) + v);
+            t[4 * v] = x.x;
+            t[4 * v + 1] = x.y;
+            t[4 * v + 2] = x.z;
+            t[4 * v + 3] = x.w;
+        }
+#pragma unroll
+        for (int j = 0; j < D; ++j) p[j] = t[j];
+        if constexpr (S > D) {
+            if (split) *split = t[S - 1];
+        }
     } else if constexpr (S == 2 && D == 2) {
         const float2 v = __ldg(reinterpret_cast<const float2*>(base));
         p[0] = v.x;
@@ -819,6 +836,7 @@ constexpr int kWalkThreads = FKD_WALK_T;
 
 template <int D, int KB>
 constexpr int walk_min_blocks() {
+    if (D > 8) return 1;  // 9..16-D: the query, its rotation, the cell offsets and the node are 4 x D registers
     return KB == 8 ? FKD_MINB_KB8 : (KB == 16 ? (D >= FKD_SLOT_LIST_MIN_D ? FKD_MINB_KB16_SLOT
                                              : (D == 5 || D == 8) ? FKD_MINB_KB16_HIGH_D : FKD_MINB_KB16)
                        : 1);

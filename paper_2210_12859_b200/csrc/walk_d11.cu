@@ -1,0 +1,8 @@
+// walk_d11.cu — 11-D kernels over the S=12 store (buckets 1/8/16/32/64).
+#include "walk_inst.cuh"
+namespace fkd {
+int launch_walk_d11(const WalkArgs& a, int S, int KB, bool stats, bool unordered, int phase, cudaStream_t st) {
+    (void)S;
+    return launch_fixed_hd<11, 12>(a, KB, stats, unordered, phase, st);
+}
+}  // namespace fkd

@@ -123,6 +123,36 @@ int launch_fixed(const WalkArgs& a, int KB, bool stats, bool unordered, int phas
     }
 }
 
+// 9..16-D: the production walk only (ordered, no counters: STATS and
+// unordered batches take the heap kernel there), buckets 1 / 8 / 16 / 32 / 64
+// (walk_bucket_of(k, dim) rounds k up to one)
+template <int D, int S, int KB>
+int launch_bucket_hd(const WalkArgs& a, bool stats, bool unordered, int phase, cudaStream_t st) {
+    if (stats || unordered) return 0;
+    if (phase == 1) {
+        if (a.budget <= 0) return 0;
+        launch_overflow<D, S, KB>(a, st);
+        return 1;
+    }
+    if (phase == 3)
+        launch_round<D, S, KB, false>(a, st);
+    else
+        launch_one<D, S, KB, false, false>(a, st);
+    return 1;
+}
+
+template <int D, int S>
+int launch_fixed_hd(const WalkArgs& a, int KB, bool stats, bool unordered, int phase, cudaStream_t st) {
+    switch (KB) {
+        case 1: return launch_bucket_hd<D, S, 1>(a, stats, unordered, phase, st);
+        case 8: return launch_bucket_hd<D, S, 8>(a, stats, unordered, phase, st);
+        case 16: return launch_bucket_hd<D, S, 16>(a, stats, unordered, phase, st);
+        case 32: return launch_bucket_hd<D, S, 32>(a, stats, unordered, phase, st);
+        case 64: return launch_bucket_hd<D, S, 64>(a, stats, unordered, phase, st);
+        default: return 0;
+    }
+}
+
 template <int D>
 int launch_heap(const WalkArgs& a, bool stats, bool unordered, cudaStream_t st) {
     const unsigned grid = walk_blocks(a.m, 128);
@@ -148,6 +178,14 @@ int launch_walk_d4(const WalkArgs&, int S, int KB, bool, bool, int phase, cudaSt
 int launch_walk_d5(const WalkArgs&, int S, int KB, bool, bool, int phase, cudaStream_t);
 int launch_walk_d6(const WalkArgs&, int S, int KB, bool, bool, int phase, cudaStream_t);
 int launch_walk_d7(const WalkArgs&, int S, int KB, bool, bool, int phase, cudaStream_t);
+int launch_walk_d9(const WalkArgs&, int S, int KB, bool, bool, int phase, cudaStream_t);
+int launch_walk_d10(const WalkArgs&, int S, int KB, bool, bool, int phase, cudaStream_t);
+int launch_walk_d11(const WalkArgs&, int S, int KB, bool, bool, int phase, cudaStream_t);
+int launch_walk_d12(const WalkArgs&, int S, int KB, bool, bool, int phase, cudaStream_t);
+int launch_walk_d13(const WalkArgs&, int S, int KB, bool, bool, int phase, cudaStream_t);
+int launch_walk_d14(const WalkArgs&, int S, int KB, bool, bool, int phase, cudaStream_t);
+int launch_walk_d15(const WalkArgs&, int S, int KB, bool, bool, int phase, cudaStream_t);
+int launch_walk_d16(const WalkArgs&, int S, int KB, bool, bool, int phase, cudaStream_t);
 int launch_walk_d8(const WalkArgs&, int S, int KB, bool, bool, int phase, cudaStream_t);
 int launch_walk_heap(const WalkArgs&, int dim, bool, bool, cudaStream_t);
 

@@ -21,7 +21,7 @@ def test_random_sweep(oracle):
     cases = 0
     while time.time() - t0 < seconds and (cases < 400 or seconds > 60):
         n = rng.next_int(1, 200_000) if rng.chance(0.3) else rng.next_int(1, 5000)
-        dim = rng.next_int(1, 10)
+        dim = rng.next_int(1, 16)
         grid = (0, 4, 8, 16, 1024)[rng.next_int(0, 4)]
         dup = (0.0, 0.05, 0.3)[rng.next_int(0, 2)]
         pts = rng.random_point_set(n, dim, grid, dup)

@@ -580,6 +580,50 @@ def test_slot_list_walk_high_dim(oracle, budget, resume_min, resume_trips, round
                     f"budgeted n={n} k={k} r={r} budget={budget}"
 
 
+@pytest.mark.parametrize("budget,rounds", [("-1", "-"), ("2", "0"), ("40", "1,2")])
+def test_register_walks_9_to_16d(oracle, budget, rounds, monkeypatch):
+    """9..16-D batches run the compile-time register walks (padded 12/16-float
+    store with the split plane, box pruning, buckets 1/8/16/32/64, Morton keys
+    over the first 8 axes, budget / rounds / CTA pass): every bucket, k below
+    the bucket, bounded radii, ties and duplicates equal the reference; STATS
+    and unordered batches (the heap kernel there) too; a non-finite last
+    coordinate rejects the batch with its index."""
+    import torch
+
+    monkeypatch.setenv("FKD_BUDGET", budget)
+    if rounds != "-":
+        monkeypatch.setenv("FKD_RROUNDS_KNN", rounds)
+        monkeypatch.setenv("FKD_RROUNDS_FCP", rounds)
+    rng = oracle.instance_rng(9016)
+    for dim in range(9, 17):
+        n = (0, 1, 7, 2500, 9000)[dim % 5]
+        pts = rng.random_point_set(n, dim, 8 if dim % 2 else 0, 0.2 if dim % 3 == 0 else 0.0)
+        nodes = (oracle.build_tree(pts) if n else pts).reshape(n, dim)
+        qs = np.stack([rng.random_query(dim, pts) for _ in range(300)])
+        tree = fk.KdTree.from_level_order(nodes)
+        for k in (0, 3, 8, 12, 16, 25, 32, 40, 64):
+            for r in (INF, 0.5):
+                what = f"dim={dim} n={n} k={k} r={r} budget={budget}"
+                opt = fk.BatchOptions(kind=_kind(k), k=max(k, 1), max_radius=r)
+                res = fk.run_batch(tree, qs, opt)
+                c, h = oracle.run_batch(nodes, qs, "knn" if k else "fcp", max(k, 1), r)[:2]
+                assert np.array_equal(res.counts, c) and res.hits.tobytes() == h.tobytes(), what
+                cd = torch.empty(len(qs), dtype=torch.int32, device="cuda")
+                hd = torch.empty(len(qs) * opt.stride, dtype=torch.int64, device="cuda")
+                fk.run_batch_device(tree, torch.from_numpy(qs).cuda(), cd, hd, opt)
+                assert np.array_equal(cd.cpu().numpy(), c) and hd.cpu().numpy().tobytes() == h.tobytes(), what
+        if n:
+            for k in (1, 8):
+                res, ref = _run_both(oracle, nodes, qs, k, INF)  # STATS: the reference's counters
+                _assert_same(res, ref, f"stats dim={dim} k={k}")
+                uo = fk.run_batch(tree, qs, fk.BatchOptions(kind=fk.QueryKind.knn, k=k, unordered=True))
+                assert np.array_equal(uo.counts, ref[0]) and uo.hits.tobytes() == ref[1].tobytes()
+            bad = qs.copy()
+            bad[77, dim - 1] = np.nan  # an axis the Morton key does not read
+            with pytest.raises(fk.DataError, match="non-finite coordinate in point 77"):
+                fk.run_batch(tree, bad, fk.BatchOptions(kind=fk.QueryKind.knn, k=8))
+
+
 def test_rejected_batch_writes_no_output(oracle, monkeypatch):
     """A non-finite query rejects the batch before any slot is written, as
     the reference throws before its BatchResult exists (batch.cpp:79 before

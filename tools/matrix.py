@@ -100,7 +100,7 @@ def run(ref, name, n, m, dim, data, batches, cpu_sample, unordered=(False,), rep
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", default="c1,c2,c3,c4,c5")
+    ap.add_argument("--only", default="c1,c2,c3,c4,c5")  # also: paper, hd
     ap.add_argument("--c5-queries", type=int, default=1_000_000_000)
     args = ap.parse_args()
     ref = Reference()
@@ -121,6 +121,10 @@ def main():
         run(ref, "paper-4D", 10_000_000, 10_000_000, 4, "uniform",
             [("fcp", 1, INF), ("knn", 4, INF), ("knn", 8, INF), ("knn", 20, INF), ("knn", 50, INF),
              ("knn", 4, 0.01), ("knn", 8, 0.01), ("knn", 20, 0.01), ("knn", 50, 0.01)], 100_000, reps=2)
+    if "hd" in only:  # beyond the BASELINE configs: 9..16-D register walks (N = M = 1M uniform)
+        for dim, sample in ((10, 20_000), (12, 10_000), (16, 2_000)):
+            run(ref, f"HD-{dim}D", 1_000_000, 1_000_000, dim, "uniform", [("fcp", 1, INF), ("knn", 8, INF)], sample,
+                reps=1)
     if "c5" in only:
         t0 = time.time()
         run(ref, "C5", 100_000_000, args.c5_queries, 3, "uniform", [("fcp", 1, INF)], 2_000_000, reps=2)
