@@ -83,9 +83,19 @@ inline bool rounds_on(int k, int64_t m, const Knobs& kn, int dim) {
 // walk to the end (M = 1M, N = 1M: 12-D kNN8 1026 -> 846 ms, 16-D 21.1 ->
 // 5.8 s; 10-D keeps the budget, 37 vs 49 ms; profiles/r02/r02bd_hd_budget_ab.log)
 constexpr int kNoBudgetDim = 12;
+// Batches of a few hundred queries walk without a budget below the long-walk
+// dims (the rounds, resume and CTA passes would be five more launches and
+// counter resets on a call whose time is launches plus its longest walk) and
+// without the Morton sort (FKD_MORTON_MIN_M): C3 tree, pinned call, M = 1 /
+// 10 / 100: fcp 82 / 108 / 117 -> 62 / 84 / 95 us, kNN8 82 / 146 / 160 -> 69 /
+// 134 / 150 us (tools/latency.py, profiles/r02/r02bf_small_batch_*.log).
+// Parking them all into the CTA pass instead is slower for kNN (160 us at M = 1).
+#ifndef FKD_SMALL_BATCH
+#define FKD_SMALL_BATCH 512
+#endif
 // first walk's loop trips before a query parks (FKD_BUDGET < 0: per kind; 0: no budget)
 inline int first_budget(int k, int64_t m, const Knobs& kn, int dim) {
-    if (dim >= kNoBudgetDim) return 0;
+    if (dim >= kNoBudgetDim || (m < FKD_SMALL_BATCH && dim < kLongWalkDim)) return 0;
     if (dim >= kLongWalkDim) return k == 1 ? 1024 : 8192;
     if (k == 1) return 112;
     if (!rounds_on(k, m, kn, dim)) return 3072;
@@ -629,10 +639,15 @@ fkd_status validate(const fkd_tree* t, int64_t m, int32_t dim, const fkd_batch_o
     return FKD_OK;
 }
 
+#ifndef FKD_MORTON_MIN_M
+#define FKD_MORTON_MIN_M 512
+#endif
 bool use_morton(const fkd_tree* t, const fkd_batch_options* o, int64_t m) {
     if (o->flags & FKD_FLAG_NO_MORTON) return false;
     if (!(o->flags & FKD_FLAG_MORTON)) return false;
-    return t->n > 0 && m > 1 && t->dim <= kMaxRegDim;  // from 9-D the key covers the first 8 axes
+    // from 9-D the key covers the first 8 axes; below FKD_MORTON_MIN_M queries
+    // the sort's launches cost more than the order saves
+    return t->n > 0 && m >= FKD_MORTON_MIN_M && t->dim <= kMaxRegDim;
 }
 
 // A Morton order computed by another batch of the same submission over the
