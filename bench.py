@@ -488,7 +488,7 @@ def run_b200(args) -> None:
             fk.LIB.fkd_host_free(hq)
         return val, same
 
-    def e2e_pipelined_run(depth: int = 2) -> tuple[float, bool]:
+    def e2e_pipelined_run(depth: int = 3) -> tuple[float, bool]:
         # a serving loop: step s+1 is submitted (fkd_submit_batches) before
         # step s is collected (fkd_wait), so one step's uploads and walks
         # overlap the previous step's result copies; every step still moves
@@ -638,7 +638,7 @@ def run_b200(args) -> None:
         line["e2e_pipelined"] = {"value": e2e_pp_value, "unit": "queries/s", "h2d_bytes_per_step": h2d,
                                  "d2h_bytes_per_step": d2h, "results_equal_device_path": bool(e2e_pp_parity),
                                  "path": "a serving loop over the same C ABI: fkd_submit_batches for step s+1 "
-                                         "before fkd_wait for step s (2 jobs in flight, one pinned buffer set each); "
+                                         "before fkd_wait for step s - 2 (3 jobs in flight, one pinned buffer set each); "
                                          "every step still uploads its queries and copies its results back"}
     if e2e_pg_value is not None:
         line["e2e_pageable"] = {"value": e2e_pg_value, "unit": "queries/s", "h2d_bytes_per_step": h2d,
