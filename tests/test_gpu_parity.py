@@ -624,6 +624,24 @@ def test_register_walks_9_to_16d(oracle, budget, rounds, monkeypatch):
                 fk.run_batch(tree, bad, fk.BatchOptions(kind=fk.QueryKind.knn, k=8))
 
 
+def test_register_walks_high_dim_against_reference(reference):
+    """9..16-D against the unmodified reference library (oracle/_ref) itself,
+    at a scale where the walks park and resume (N = 200k, 4000 queries from the
+    reference's own generator): fcp, kNN 8 / 16 / 40, unbounded and bounded
+    radii — counts, hit nodes and dist2 bits, and the reference's result hash."""
+    for dim in (9, 11, 12, 16):
+        pts = reference.stream_points(3, 1, 200_000, dim)
+        nodes = reference.build_tree(pts)
+        qs = reference.stream_points(3, 2, 4000 if dim < 16 else 1000, dim)  # the reference's 16-D walks are long
+        tree = fk.KdTree.from_level_order(nodes)
+        for kind, k, r in (("fcp", 1, INF), ("knn", 8, INF), ("knn", 16, 0.4), ("knn", 40, INF)):
+            c, h, _, _ = reference.run_batch(nodes, qs, kind, k, r)
+            got = fk.run_batch(tree, qs, fk.BatchOptions(kind=fk.QueryKind[kind], k=k, max_radius=r))
+            what = f"dim={dim} {kind} k={k} r={r}"
+            assert np.array_equal(got.counts, c) and got.hits.tobytes() == h.tobytes(), what
+            assert got.result_hash() == reference.result_hash(c, h, k if kind == "knn" else 1), what
+
+
 def test_rejected_batch_writes_no_output(oracle, monkeypatch):
     """A non-finite query rejects the batch before any slot is written, as
     the reference throws before its BatchResult exists (batch.cpp:79 before
