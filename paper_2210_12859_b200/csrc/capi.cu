@@ -837,7 +837,6 @@ fkd_status enqueue(const fkd_tree* t, Replica& r, Workspace* w, const float* d_q
 
 }  // namespace
 
-int walk_bucket(int k) { return walk_bucket_of(k); }
 
 int launch_walk(const WalkArgs& a, int dim, int stride, bool stats, bool unordered, int phase,
                 cudaStream_t st) {

@@ -1120,7 +1120,5 @@ __global__ void __launch_bounds__(128) walk_heap_kernel(const WalkArgs a) {
 int launch_walk(const WalkArgs& a, int dim, int layout_stride, bool stats, bool unordered,
                 int phase, cudaStream_t stream);
 
-// Register-list capacity used for k (0 = heap kernel).
-int walk_bucket(int k);
 
 }  // namespace fkd
