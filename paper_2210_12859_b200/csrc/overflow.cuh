@@ -210,7 +210,7 @@ __global__ void __launch_bounds__(THREADS) overflow_kernel(const WalkArgs a) {
                 for (int j = 0; j < C; ++j) rank += key_lt(cand[j], x);
                 if (rank < k)
                     reinterpret_cast<int2*>(a.hits + qi * k)[rank] =
-                        make_int2(int32_t(uint32_t(x)), int32_t(uint32_t(x >> 32) - 1u));
+                        make_int2(int32_t(uint32_t(x)), int32_t(uint32_t(x >> 32) - kKeyOfs));
             }
             for (int j = C + tid; j < k; j += THREADS)  // fewer than k admissible: Hit{-1, +inf}
                 reinterpret_cast<int2*>(a.hits + qi * k)[j] = make_int2(-1, 0x7f800000);
@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(THREADS) overflow_kernel(const WalkArgs a) {
                 if (h == w && w != kEmptyKey) list_pop(L, dummies);
                 if (tid == 0) {
                     reinterpret_cast<int2*>(a.hits + qi * k)[j] =
-                        make_int2(int32_t(uint32_t(w)), int32_t(uint32_t(w >> 32) - 1u));
+                        make_int2(int32_t(uint32_t(w)), int32_t(uint32_t(w >> 32) - kKeyOfs));
                     if (j == 0) fcount[0] = 0;
                     if (w != kEmptyKey) ++fcount[0];  // reuse as the hit counter
                 }

@@ -105,7 +105,7 @@ __global__ void trace_kernel(const float* __restrict__ nodes, int32_t n, int dim
     int2* out = reinterpret_cast<int2*>(heap);
     for (int j = 0; j < k; ++j) {
         const uint64_t key = j < count ? heap[j] : kEmptyKey;
-        out[j] = make_int2(int32_t(uint32_t(key)), int32_t(uint32_t(key >> 32) - 1u));
+        out[j] = make_int2(int32_t(uint32_t(key)), int32_t(uint32_t(key >> 32) - kKeyOfs));
     }
     counts[qi] = count;
     stats[qi] = fkd_query_stats{steps, visited, processed};

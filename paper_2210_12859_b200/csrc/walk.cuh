@@ -37,7 +37,17 @@
 
 namespace fkd {
 
-constexpr uint64_t kEmptyKey = (uint64_t(0x7f800000u + 1u) << 32) | 0xFFFFFFFFull;
+// Key = (bits(d2) + kKeyOfs) << 32 | node.  With the offset 0 (default) the
+// high word is the distance's own bits, so forming a key and reading a
+// radius back cost no add: one instruction less per walk trip (C3 step 9.33
+// -> 9.21 ms, 8-D kNN16 -4.5%; profiles/r02/r02bn_key_offset_ab.log).  A real
+// key may then equal the dummy key 0 (d2 = +0 at node 0): the insertion puts
+// it after the dummies (x < 0 is false), and dummies are skipped by index.
+#ifndef FKD_KEY_OFS
+#define FKD_KEY_OFS 0
+#endif
+constexpr uint32_t kKeyOfs = FKD_KEY_OFS;
+constexpr uint64_t kEmptyKey = (uint64_t(0x7f800000u + kKeyOfs) << 32) | 0xFFFFFFFFull;
 constexpr uint64_t kNoBad = ~0ull;
 
 // Block timeline instrumentation (profiling builds only: -DFKD_BLOCK_TRACE=1;
@@ -117,11 +127,11 @@ struct BlockTrace {
 };
 
 __device__ __forceinline__ uint64_t make_key(float d2, int32_t node) {
-    return (uint64_t(__float_as_uint(d2) + 1u) << 32) | uint32_t(node);
+    return (uint64_t(__float_as_uint(d2) + kKeyOfs) << 32) | uint32_t(node);
 }
 
 __device__ __forceinline__ float key_dist(uint64_t key) {
-    return __uint_as_float(uint32_t(key >> 32) - 1u);
+    return __uint_as_float(uint32_t(key >> 32) - kKeyOfs);
 }
 
 // Empty slot of a register list: the admission cap's own key with node
@@ -131,7 +141,7 @@ __device__ __forceinline__ float key_dist(uint64_t key) {
 // key_dist(L[KB-1]): cap2 while the list is short, the kth distance once it
 // is full (traverse.hpp:97, 135-137).  With cap2 = +inf this is kEmptyKey.
 __device__ __forceinline__ uint64_t cap_key(float cap2) {
-    return (uint64_t(__float_as_uint(cap2) + 1u) << 32) | 0xFFFFFFFFull;
+    return (uint64_t(__float_as_uint(cap2) + kKeyOfs) << 32) | 0xFFFFFFFFull;
 }
 
 __device__ __forceinline__ int32_t depth_of(int32_t node) {  // tree.hpp:20-22
@@ -259,12 +269,11 @@ __device__ __forceinline__ void load_point(const float* __restrict__ nodes, int3
     }
 }
 
-// Key order on the FP64 compare.  A key is ((bits(d2) + 1) << 32) | node
-// with d2 in [0, +inf] (queries and tree are finite; cap2 is not NaN), so its
-// sign bit is 0 and its high word is <= 0x7F800001: read as an IEEE double it
-// is finite and non-negative, and non-negative doubles order exactly like
-// their bit patterns (FP64 never flushes subnormals; +0 is only the dummy
-// key 0).  One DSETP replaces the two-instruction 64-bit ISETP pair and runs
+// Key order on the FP64 compare.  A key is (bits(d2) << 32) | node with d2 in
+// [0, +inf] (queries and tree are finite; cap2 is not NaN), so its sign bit
+// is 0 and its high word is <= 0x7F800000: read as an IEEE double it is
+// finite and non-negative, and non-negative doubles order exactly like their
+// bit patterns (FP64 never flushes subnormals, which keys with d2 = 0 are).  One DSETP replaces the two-instruction 64-bit ISETP pair and runs
 // on the FP64 pipe instead of the ALU pipe the walk saturates; and since the
 // selects that follow are integer, ptxas cannot re-form a min/max idiom with
 // compares of its own.  (B200-specific: sm_100 has a full-rate-class FP64
@@ -663,11 +672,11 @@ struct LaneWalk {
         uint64_t last = x;
         for (int j = 0; j < k; ++j) {
             const int2 h = out[j];
-            const uint64_t kj = h.x < 0 ? empty : (uint64_t(uint32_t(h.y) + 1u) << 32) | uint32_t(h.x);
+            const uint64_t kj = h.x < 0 ? empty : (uint64_t(uint32_t(h.y) + kKeyOfs) << 32) | uint32_t(h.x);
             last = kj;
             if (key_lt(x, kj)) {
                 const bool hit = uint32_t(x) != 0xFFFFFFFFu;
-                out[j] = make_int2(int32_t(uint32_t(x)), hit ? int32_t(uint32_t(x >> 32) - 1u) : 0x7f800000);
+                out[j] = make_int2(int32_t(uint32_t(x)), hit ? int32_t(uint32_t(x >> 32) - kKeyOfs) : 0x7f800000);
                 last = x;
                 x = kj;
             }
@@ -689,7 +698,7 @@ struct LaneWalk {
         const int2* slot = reinterpret_cast<const int2*>(a.hits + size_t(qi) * a.k);
         if constexpr (kSlot) {
             const int2 h = slot[a.k - 1];  // the list stays in the slot; only its kth is a register
-            L[0] = h.x < 0 ? empty : (uint64_t(uint32_t(h.y) + 1u) << 32) | uint32_t(h.x);
+            L[0] = h.x < 0 ? empty : (uint64_t(uint32_t(h.y) + kKeyOfs) << 32) | uint32_t(h.x);
         } else {
 #pragma unroll
             for (int j = 0; j < KB; ++j) {
@@ -697,7 +706,7 @@ struct LaneWalk {
                     L[j] = 0ull;
                 } else {
                     const int2 h = slot[j - dummies];
-                    L[j] = h.x < 0 ? empty : (uint64_t(uint32_t(h.y) + 1u) << 32) | uint32_t(h.x);
+                    L[j] = h.x < 0 ? empty : (uint64_t(uint32_t(h.y) + kKeyOfs) << 32) | uint32_t(h.x);
                 }
             }
         }
@@ -752,7 +761,7 @@ struct LaneWalk {
                     const uint64_t key = L[j];
                     const bool hit = uint32_t(key) != 0xFFFFFFFFu;  // empty slot -> Hit{-1, +inf}
                     const int2 h = make_int2(int32_t(uint32_t(key)),
-                                             hit ? int32_t(uint32_t(key >> 32) - 1u) : 0x7f800000);
+                                             hit ? int32_t(uint32_t(key >> 32) - kKeyOfs) : 0x7f800000);
                     if (kStreamIO && final)
                         __stcs(out + s, h);
                     else
@@ -1094,7 +1103,7 @@ __global__ void __launch_bounds__(128) walk_heap_kernel(const WalkArgs a) {
         int2* out = reinterpret_cast<int2*>(heap);
         for (int j = 0; j < k; ++j) {
             const uint64_t key = j < count ? heap[j] : kEmptyKey;
-            out[j] = make_int2(int32_t(uint32_t(key)), int32_t(uint32_t(key >> 32) - 1u));
+            out[j] = make_int2(int32_t(uint32_t(key)), int32_t(uint32_t(key >> 32) - kKeyOfs));
         }
         a.counts[qi] = count;
         if constexpr (STATS) {
