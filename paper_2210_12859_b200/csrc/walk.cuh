@@ -372,6 +372,16 @@ __device__ __forceinline__ int dim_down(int d) {  // split dim one level up
 #ifndef FKD_STREAM_QUERY_LOADS
 #define FKD_STREAM_QUERY_LOADS 1
 #endif
+// Nodes of one 16-byte vector without a plane slot (4-D): every trip loads
+// the whole node.  The split-coordinate-only load of a return trip needed its
+// own address form and a branch around the two loads, and ptxas rebuilt the
+// store pointer from uniform registers on both sides each trip: 4-D kNN8 312
+// -> 287 SASS per 4 steps, walk -10% (fcp -10%, kNN4 -13%, kNN50 -6%;
+// profiles/r02/r02bt_full_return_load_ab.log).  8-D nodes (two vectors) keep
+// the scalar load: +3% SASS the other way.
+#ifndef FKD_FULL_RETURN_LOAD
+#define FKD_FULL_RETURN_LOAD 1
+#endif
 #ifndef FKD_STREAM_IO_MIN_KB
 #define FKD_STREAM_IO_MIN_KB 8
 #endif
@@ -495,7 +505,12 @@ struct LaneWalk {
         const float* nodes = a.nodes - S;  // nodes + c * S is 1-based node c's slot
         float p[D];
         float pd;
-        if constexpr (S == D && D > 1) {
+        if constexpr (S == D && D > 1 && S <= 4 && FKD_FULL_RETURN_LOAD) {
+            // one vector load on every trip (a return trip's plane is in the same
+            // sector): no second address form, no branch around the loads
+            load_point<D, S>(nodes, curr, p);
+            pd = pick(p, d);
+        } else if constexpr (S == D && D > 1) {
             if (from_parent) {
                 load_point<D, S>(nodes, curr, p);
                 pd = pick(p, d);
