@@ -377,10 +377,14 @@ __device__ __forceinline__ int dim_down(int d) {  // split dim one level up
 // own address form and a branch around the two loads, and ptxas rebuilt the
 // store pointer from uniform registers on both sides each trip: 4-D kNN8 312
 // -> 287 SASS per 4 steps, walk -10% (fcp -10%, kNN4 -13%, kNN50 -6%;
-// profiles/r02/r02bt_full_return_load_ab.log).  8-D nodes (two vectors) keep
-// the scalar load: +3% SASS the other way.
+// profiles/r02/r02bt_full_return_load_ab.log).  8-D nodes (two vectors, one
+// sector) too: kNN8 -9%, fcp -7%, kNN32 -5%, except the 16-slot walks whose
+// list lives in the output slot (+4%; r02bu_full_return_load8_ab.log).
 #ifndef FKD_FULL_RETURN_LOAD
 #define FKD_FULL_RETURN_LOAD 1
+#endif
+#ifndef FKD_FULL_RETURN_LOAD_MAX_S
+#define FKD_FULL_RETURN_LOAD_MAX_S 8
 #endif
 #ifndef FKD_STREAM_IO_MIN_KB
 #define FKD_STREAM_IO_MIN_KB 8
@@ -505,7 +509,7 @@ struct LaneWalk {
         const float* nodes = a.nodes - S;  // nodes + c * S is 1-based node c's slot
         float p[D];
         float pd;
-        if constexpr (S == D && D > 1 && S <= 4 && FKD_FULL_RETURN_LOAD) {
+        if constexpr (S == D && D > 1 && S <= FKD_FULL_RETURN_LOAD_MAX_S && !kSlot && FKD_FULL_RETURN_LOAD) {
             // one vector load on every trip (a return trip's plane is in the same
             // sector): no second address form, no branch around the loads
             load_point<D, S>(nodes, curr, p);
