@@ -386,6 +386,12 @@ __device__ __forceinline__ int dim_down(int d) {  // split dim one level up
 #ifndef FKD_FULL_RETURN_LOAD_MAX_S
 #define FKD_FULL_RETURN_LOAD_MAX_S 8
 #endif
+// Packed-pair distance (FADD2/FMUL2) for 2-/3-D lists of any length (4-D
+// keeps it to <= 8 slots): 2-D kNN16 -1.3%, 3-D kNN16 -3%, kNN50 -1%
+// (profiles/r02/r02bz_pair_any_kb_ab.log)
+#ifndef FKD_PAIR_ANY_KB_MAX_D
+#define FKD_PAIR_ANY_KB_MAX_D 3
+#endif
 #ifndef FKD_STREAM_IO_MIN_KB
 #define FKD_STREAM_IO_MIN_KB 8
 #endif
@@ -539,7 +545,7 @@ struct LaneWalk {
             // 3-D -3.6% with the packed-pair distance, but 4-D +22%, and the
             // 2-D fcp walk would take 44 instead of 28 registers),
             // admission is predicated on a first visit.
-            const float d2 = sq_dist<D, (D <= 4 && KB <= 8)>(q, p);
+            const float d2 = sq_dist<D, ((D <= 4 && KB <= 8) || D <= FKD_PAIR_ANY_KB_MAX_D)>(q, p);
             const uint64_t key = make_key(d2, curr - 1 + int32_t(kNodeOfs));
             if constexpr (kSlot) {
                 if (from_parent && key_lt(key, L[0])) {
@@ -551,7 +557,7 @@ struct LaneWalk {
                 r2 = key_dist(L[KB - 1]);
             }
         } else if (from_parent) {  // fcp, D != 3: a branch is cheaper than the FP ops
-            const float d2 = sq_dist<D, (D <= 4 && KB <= 8)>(q, p);
+            const float d2 = sq_dist<D, ((D <= 4 && KB <= 8) || D <= FKD_PAIR_ANY_KB_MAX_D)>(q, p);
             const uint64_t key = make_key(d2, curr - 1 + int32_t(kNodeOfs));
             if constexpr (kSlot) {
                 if (key_lt(key, L[0])) {
