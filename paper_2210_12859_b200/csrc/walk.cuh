@@ -386,12 +386,10 @@ __device__ __forceinline__ int dim_down(int d) {  // split dim one level up
 #ifndef FKD_FULL_RETURN_LOAD_MAX_S
 #define FKD_FULL_RETURN_LOAD_MAX_S 8
 #endif
-// Packed-pair distance (FADD2/FMUL2) for 2-/3-D lists of any length (4-D
-// keeps it to <= 8 slots): 2-D kNN16 -1.3%, 3-D kNN16 -3%, kNN50 -1%
-// (profiles/r02/r02bz_pair_any_kb_ab.log)
-#ifndef FKD_PAIR_ANY_KB_MAX_D
-#define FKD_PAIR_ANY_KB_MAX_D 3
-#endif
+// Packed-pair distance (FADD2/FMUL2, LaneWalk::kPairDist): 2-/3-D lists of any
+// length and 4-D lists of up to 32 slots (round 1 stopped at 8 slots): 2-D
+// kNN16 -1.3%, 3-D kNN16 -3%, kNN50 -1%, 4-D kNN16 -4%, kNN20 -3%, kNN32 -2%;
+// 4-D kNN50 +7% (profiles/r02/r02bz_pair_any_kb_ab.log, r02ca_pair4d_ab.log)
 #ifndef FKD_STREAM_IO_MIN_KB
 #define FKD_STREAM_IO_MIN_KB 8
 #endif
@@ -431,6 +429,7 @@ struct LaneWalk {
     // coordinate split at the current depth (rotated by one per level).
     static constexpr bool kRot = S > D && D > 1;
     static constexpr int kKB = KB;
+    static constexpr bool kPairDist = D <= 3 || (D == 4 && KB <= 32);
     static constexpr uint32_t kNodeOfs = KB == 1 ? FKD_FCP_KEY_NODE_OFS : 0;  // key low word = node + kNodeOfs
     static constexpr bool kStreamIO = KB >= FKD_STREAM_IO_MIN_KB;
     static constexpr int kD = D;
@@ -545,7 +544,7 @@ struct LaneWalk {
             // 3-D -3.6% with the packed-pair distance, but 4-D +22%, and the
             // 2-D fcp walk would take 44 instead of 28 registers),
             // admission is predicated on a first visit.
-            const float d2 = sq_dist<D, ((D <= 4 && KB <= 8) || D <= FKD_PAIR_ANY_KB_MAX_D)>(q, p);
+            const float d2 = sq_dist<D, kPairDist>(q, p);
             const uint64_t key = make_key(d2, curr - 1 + int32_t(kNodeOfs));
             if constexpr (kSlot) {
                 if (from_parent && key_lt(key, L[0])) {
@@ -557,7 +556,7 @@ struct LaneWalk {
                 r2 = key_dist(L[KB - 1]);
             }
         } else if (from_parent) {  // fcp, D != 3: a branch is cheaper than the FP ops
-            const float d2 = sq_dist<D, ((D <= 4 && KB <= 8) || D <= FKD_PAIR_ANY_KB_MAX_D)>(q, p);
+            const float d2 = sq_dist<D, kPairDist>(q, p);
             const uint64_t key = make_key(d2, curr - 1 + int32_t(kNodeOfs));
             if constexpr (kSlot) {
                 if (key_lt(key, L[0])) {
