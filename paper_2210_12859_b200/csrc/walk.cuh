@@ -390,6 +390,11 @@ __device__ __forceinline__ int dim_down(int d) {  // split dim one level up
 // length and 4-D lists of up to 32 slots (round 1 stopped at 8 slots): 2-D
 // kNN16 -1.3%, 3-D kNN16 -3%, kNN50 -1%, 4-D kNN16 -4%, kNN20 -3%, kNN32 -2%;
 // 4-D kNN50 +7% (profiles/r02/r02bz_pair_any_kb_ab.log, r02ca_pair4d_ab.log)
+// ... and 5..16-D lists of up to 16 slots: 8-D fcp -4%, kNN8 -1.5%, 6-D kNN8
+// -3%, 10-D kNN8 -1.5 to -4%, 5-D and 8-D kNN16 within 1% (r02cb_pair_hd_ab.log)
+#ifndef FKD_PAIR_HD
+#define FKD_PAIR_HD 1
+#endif
 #ifndef FKD_STREAM_IO_MIN_KB
 #define FKD_STREAM_IO_MIN_KB 8
 #endif
@@ -429,7 +434,7 @@ struct LaneWalk {
     // coordinate split at the current depth (rotated by one per level).
     static constexpr bool kRot = S > D && D > 1;
     static constexpr int kKB = KB;
-    static constexpr bool kPairDist = D <= 3 || (D == 4 && KB <= 32);
+    static constexpr bool kPairDist = D <= 3 || (D == 4 && KB <= 32) || (FKD_PAIR_HD && D >= 5 && D <= 16 && KB <= 16);
     static constexpr uint32_t kNodeOfs = KB == 1 ? FKD_FCP_KEY_NODE_OFS : 0;  // key low word = node + kNodeOfs
     static constexpr bool kStreamIO = KB >= FKD_STREAM_IO_MIN_KB;
     static constexpr int kD = D;
